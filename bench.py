@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: cell-updates/s (fp64, 3D Sedov) of the telescoped SSP-RK2 hydro
+step (BASELINE.json metric), one process per GPU.
+
+Workload (BASELINE.json configs[3], "3D Sedov weak scaling, 4096 blocks of
+16^3 cells per GPU at 1/2/4/8 B200 with NCCL halo exchange + dt allreduce"):
+every rank owns a brick of 16x16x16 blocks of 16^3 cells (256^3 cells,
+dx = 1/256) arranged on a GPU grid (1,1,1), (2,1,1), (2,2,1), (2,2,2); the
+Sedov blast sits at the global centre.  A step is one pass
+of the whole hot path: guard fill (+ halo exchange) -> CFL dt (+ allreduce)
+-> telescoped RK2 advance of the packet.  Inputs (2.2 GB state per GPU) are
+far larger than the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BRICK_BLOCKS = (16, 16, 16)
+NB = (16, 16, 16)
+GPU_GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+METRIC = "cell-updates/sec (fp64, 3D Sedov)"
+UNIT = "cell-updates/s"
+
+
+def algorithmic_costs(nb=16, ng=4):
+    """Per cell-update algorithmic work of the telescoped 16^3 step (DESIGN.md
+    'Roofline'): bytes of the advance (read the padded block once, write the
+    interior once) and of the guard fill (read sources, write guards); fp64
+    flops of the method with every face flux, EOS and slope evaluated once."""
+    P = nb + 2 * ng
+    n3 = nb ** 3
+    adv_bytes = (P ** 3 + n3) * 5 * 8 / n3
+    guards = P ** 3 - n3
+    fill_bytes = 2 * guards * 5 * 8 / n3
+    # faces: stage 1 on the box (n+4)^3 (x-faces (n+5)(n+4)^2 per axis), stage 2 on n^3
+    s1 = nb + 4
+    faces = 3 * (s1 + 1) * s1 * s1 + 3 * (nb + 1) * nb * nb
+    cells_eos = P ** 3 + s1 ** 3          # primitive recovery of stage-1 input, stage-2 input
+    slopes = 3 * ((s1 + 2) * s1 * s1 + (nb + 2) * nb * nb)  # per axis per cell of the face stencils
+    flops = (faces * FLOPS_PER_FACE + cells_eos * FLOPS_PER_EOS + slopes * 5 * FLOPS_PER_SLOPE +
+             (s1 ** 3 + n3) * 5 * FLOPS_PER_UPDATE) / n3
+    return adv_bytes, fill_bytes, flops
+
+
+# fp64 flop counts of the method's expressions (FMA counted as 2; div, sqrt as 1)
+FLOPS_PER_FACE = 2 * 5 + 2 * (3 + 9 + 5 + 2) + 6 + 1 + 1 + 5 * 6   # PLM faces, 2x(c,E,U,F), S_L/S_R, inv, HLL
+FLOPS_PER_EOS = 12
+FLOPS_PER_SLOPE = 5
+FLOPS_PER_UPDATE = 5                                                 # dF*id sums + RK combination
+
+
+def peaks():
+    p = {"hbm_gbs": 6535.4, "source": "fallback (B200_PROFILING.md earlier pool measurement is 6650; "
+                                      "MEASURED_PEAKS.json absent)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        m = json.load(open(path))
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)",
+             "sm_max_mhz": float(m.get("sm_max_mhz", 1965.0))}
+    # fp64 pipe: 148 SMs x 64 fp64 FMA lanes x 2 flop x clock (B200_PROFILING.md unit counts)
+    p["fp64_tflops"] = 148 * 64 * 2 * p.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/orcha_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+# ------------------------------------------------------------------ reference
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores, one
+    bounded sample of the workload per step (a 64^3 sub-box of the same Sedov
+    setup: ghost fill, dt, one telescoped RK2 step)."""
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+
+    import oracle
+    import orcha_inputs as inp
+
+    n = 64
+    og = oracle.Grid(N=(n, n, n))
+    U0 = inp.sedov((n, n, n))
+    U = oracle.padded(og, U0)
+
+    def one_step():
+        oracle.fill_ghosts(og, U)
+        r = oracle.compute_dt(og, U)
+        oracle.step(og, U, r.dt)
+
+    for _ in range(args.warmup):
+        one_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    el = time.perf_counter() - t0
+    ms = el / args.steps * 1e3
+    value = n ** 3 * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg4 3D Sedov (oracle sample: 64^3 sub-box per step)", "global_batch": None,
+                       "seq_len": None, "parallelism": "cpu oracle, 1 thread"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"64^3 3D Sedov, {args.steps} timed steps (plain C oracle, -O2 -ffp-contract=off)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(seconds_target=15.0):
+    """The oracle as it stands on this host (1 thread), on a bounded sample of
+    the workload: a 128^3 sub-box of the 3D Sedov setup, as many steps as fit
+    ~15 s (at least 1)."""
+    import oracle
+    import orcha_inputs as inp
+
+    n = 96
+    og = oracle.Grid(N=(n, n, n))
+    U = oracle.padded(og, inp.sedov((n, n, n)))
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        oracle.fill_ghosts(og, U)
+        r = oracle.compute_dt(og, U)
+        oracle.step(og, U, r.dt)
+        steps += 1
+        if time.perf_counter() - t0 > seconds_target:
+            break
+    el = time.perf_counter() - t0
+    return {"value": n ** 3 * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n}^3 3D Sedov sub-box, {steps} steps (fill+dt+RK2), {el:.1f} s, 1 thread"}
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="orcha", choices=["orcha", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=None, help="advance kernel variant (0 ref, 1 fused)")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import orcha_inputs as inp
+    from paper_2507_09337_b200 import abi, build, hydro
+
+    if world != args.gpus:
+        args.gpus = world
+    if world not in GPU_GRIDS:
+        raise SystemExit(f"--gpus must be one of {sorted(GPU_GRIDS)}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0 and not os.path.exists(abi.library_path(False)):
+        build.build()
+    if world > 1:
+        dist.barrier()
+    lib = abi.load(False)
+    if args.variant is not None:
+        hydro.set_kernel_variant(lib, args.variant)
+
+    px, py, pz = GPU_GRIDS[world]
+    nblk = (BRICK_BLOCKS[0] * px, BRICK_BLOCKS[1] * py, BRICK_BLOCKS[2] * pz)
+    N = tuple(nblk[a] * NB[a] for a in range(3))
+    g = hydro.Grid(3, NB, nblk, xmin=(0.0, 0.0, 0.0), xmax=(float(px), float(py), float(pz)))
+    # this rank's brick (block ids in natural order inside the brick)
+    rx, ry, rz = rank % px, (rank // px) % py, rank // (px * py)
+    bi = np.arange(BRICK_BLOCKS[0]) + rx * BRICK_BLOCKS[0]
+    bj = np.arange(BRICK_BLOCKS[1]) + ry * BRICK_BLOCKS[1]
+    bk = np.arange(BRICK_BLOCKS[2]) + rz * BRICK_BLOCKS[2]
+    ids = ((bk[:, None, None] * nblk[1] + bj[None, :, None]) * nblk[0] + bi[None, None, :]).reshape(-1)
+    comm = None
+    if world > 1:
+        comm = hydro.Comm.create(g, world, rank, hydro.brick_owner(nblk, BRICK_BLOCKS, GPU_GRIDS[world]))
+    pk = hydro.Packet(g, ids)
+    # initial Sedov state of this brick (host, closed form) -> pinned -> pack
+    U0 = inp.sedov(N, xmax=(float(px), float(py), float(pz)))
+    host = torch.from_numpy(inp.to_blocks(U0, NB, ids)).pin_memory()
+    del U0
+    stream = torch.cuda.current_stream()
+    pk.pack(host, stream)
+    stream.synchronize()
+
+    adv_ev = []
+
+    def step(record=False):
+        hydro.orcha_fill_guardcells([pk], comm, stream)
+        info = hydro.orcha_compute_dt([pk], math.inf, comm, stream)
+        if record:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        hydro.orcha_hydro_advance(pk, info.dt, stream)
+        if record:
+            b.record(stream)
+            adv_ev.append((a, b))
+        return info
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = lib.orcha_launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.orcha_launch_count() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    cells = N[0] * N[1] * N[2]
+    value = cells / (ms / 1e3)
+    adv_ms = statistics.mean(a.elapsed_time(b) for a, b in adv_ev)
+
+    # roofline of the dominant kernel (the advance): algorithmic bytes / flops
+    pks = peaks()
+    adv_bytes, fill_bytes, flops = algorithmic_costs()
+    cu_local = BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2] * NB[0] * NB[1] * NB[2]
+    hbm_achieved = adv_bytes * cu_local / (adv_ms / 1e3) / 1e9
+    fp_achieved = flops * cu_local / (adv_ms / 1e3) / 1e12
+    roof_hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": pks["hbm_gbs"], "unit": "GB/s",
+                "frac": hbm_achieved / pks["hbm_gbs"], "traffic": None, "peak_source": pks["source"],
+                "kernel": "hydro_advance (stage1+stage2)", "algorithmic_bytes_per_cell_update": adv_bytes}
+    roof_fp = {"bound": "alu", "achieved": fp_achieved, "peak": pks["fp64_tflops"], "unit": "TFLOP/s",
+               "frac": fp_achieved / pks["fp64_tflops"], "traffic": None,
+               "peak_source": "derived: 148 SM x 64 fp64 lanes x 2 x sm_max clock",
+               "kernel": "hydro_advance (stage1+stage2)", "algorithmic_flops_per_cell_update": flops}
+    primary, other = (roof_fp, roof_hbm) if roof_fp["frac"] >= roof_hbm["frac"] else (roof_hbm, roof_fp)
+    step_hbm = (adv_bytes + fill_bytes) * value / world / 1e9
+
+    # end to end through the public API with host buffers (the paper's model:
+    # the packet is shipped H2D, advanced and shipped back every cycle)
+    e2e = None
+    if args.e2e_steps > 0:
+        out = torch.empty_like(host).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.e2e_steps):
+            pk.pack(host, stream)
+            step()
+            pk.unpack(out, stream)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ems = s0.elapsed_time(s1) / args.e2e_steps
+        te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ems = float(te.item())
+        nbytes = host.numel() * 8
+        e2e = {"value": cells / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes + 8, "ms_per_step": ems,
+               "note": "per step: pack (H2D, pinned) -> fill -> dt (D2H 8 B) -> advance -> unpack (D2H, pinned)"}
+
+    fh, bad = pk.counters(stream)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (closed-form Sedov IC)",
+            "config": {"workload": "cfg4: 3D Sedov, 4096 blocks of 16^3 (+4 guards) per GPU, one packet",
+                       "global_cells": list(N), "blocks_per_gpu": int(len(ids)), "gpu_grid": list(GPU_GRIDS[world]),
+                       "ng": 4, "gamma": 1.4, "cfl": 0.4, "l2_flush": "not needed: 2.2 GB state per GPU >> 126 MB L2",
+                       "kernel_variant": int(lib.orcha_get_kernel_variant()),
+                       "global_batch": None, "seq_len": None, "parallelism": f"blocks over {world} GPU(s)"},
+            "roofline": primary, "roofline_other": other,
+            "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
+                                       "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},
+            "advance_ms": adv_ms, "clocks": clk, "gpu_launches": int(launches), "e2e": e2e,
+            "floor_hits": fh, "nonphysical_first_cell": bad,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

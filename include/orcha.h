@@ -1,0 +1,239 @@
+/*
+ * orcha.h -- C ABI of liborcha.so: the per-block explicit hydrodynamics update
+ * that ORCHA orchestrates in its Flash-X Sedov case study (arXiv 2507.09337),
+ * applied to a data packet of N equal blocks with guard cells, on one B200.
+ *
+ * Citations: P:Lnn = PAPER.md line nn (section in parentheses); SURVEY 8(x) =
+ * the normative reading of the paper in SURVEY.md section 8 (the paper does
+ * not name the reconstruction, Riemann solver, CFL rule or boundaries; see
+ * DESIGN.md "Readings").
+ *
+ * Conventions for every call
+ *   - Return value: ORCHA_OK (0) or a negative orcha_status.  On error,
+ *     orcha_last_error() returns a thread-local, human-readable message.
+ *     Argument errors are detected synchronously, before anything is queued.
+ *   - Handles (orcha_grid, orcha_packet, orcha_comm) are opaque and owned by
+ *     the library; destroy them with the matching *_destroy call.
+ *   - Device buffers passed in (d_state, d_scratch) are OWNED BY THE CALLER
+ *     (e.g. torch tensors), must stay alive while the packet exists, and are
+ *     never freed by the library.  They must be 256-byte aligned.
+ *   - Host arrays are owned by the caller and are only read/written during
+ *     the call (or, for the async pack/unpack, until the stream reaches the
+ *     copy; use pinned memory for overlap).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream), e.g.
+ *     torch.cuda.current_stream().cuda_stream.  All device work of a call is
+ *     enqueued on it.  A packet is used by one stream at a time.
+ *   - Floating point is IEEE fp64 throughout; no fast-math.
+ *
+ * Data layout ("DataPacket", sec 4.3: "n AMR blocks" flattened into
+ * one buffer; blocks per P:L567-569 sec 5.1: "each block has the same number
+ * of cells"):
+ *   state[slot][var][k][j][i], var = (rho, rho*u, rho*v, rho*w, E), always 5
+ *   (inactive momenta are 0), padded extents nb_d + 2*ng on active axes and 1
+ *   on inactive axes, i fastest; every (slot, var) cube starts on a 256-byte
+ *   boundary (cube stride = cells*8 rounded up to 256 bytes).  Slot s holds
+ *   global block block_ids[s]; global block id b = (bk*NBy + bj)*NBx + bi and
+ *   global cell index g = (k*Ny + j)*Nx + i.
+ */
+#ifndef ORCHA_H
+#define ORCHA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ORCHA_OK = 0,
+  ORCHA_E_ARG = -1,         /* invalid argument / descriptor */
+  ORCHA_E_RANGE = -2,       /* block id or slot out of range, duplicate block, neighbour not resident */
+  ORCHA_E_HALO = -3,        /* ng < 4: the telescoped step needs a twice-thick halo */
+  ORCHA_E_NONPHYSICAL = -4, /* rho <= 0 or non-finite state met on the device (sticky, see below) */
+  ORCHA_E_LAYOUT = -5,      /* buffer misaligned or too small */
+  ORCHA_E_CUDA = -6,        /* CUDA runtime error (message has the CUDA error string) */
+  ORCHA_E_NCCL = -7,        /* NCCL error */
+  ORCHA_E_STATE = -8        /* call order violated, e.g. advance without a guard fill */
+} orcha_status;
+
+enum { ORCHA_BC_OUTFLOW = 0, ORCHA_BC_PERIODIC = 1, ORCHA_BC_REFLECT = 2 };
+enum { ORCHA_DT_CFL = 0, ORCHA_DT_CLAMP = 1 };
+
+/* Global uniform grid of equal blocks.  Boundary conditions per axis and side
+ * (SURVEY 8(c) c6): outflow = copy of the edge cell; periodic = wrap; reflect =
+ * mirror with the normal momentum negated.  Physical extent [xmin, xmax] per
+ * axis, cell size dx_d = (xmax_d - xmin_d) / (nblk_d * nb_d). */
+typedef struct {
+  int32_t ndim;       /* 1, 2 or 3 */
+  int32_t nb[3];      /* cells per block per axis (nxb, nyb, nzb); 1 on inactive axes */
+  int32_t ng;         /* guard cells per side on active axes; must be >= 4 */
+  int32_t nblk[3];    /* blocks per axis of the GLOBAL grid; 1 on inactive axes */
+  double xmin[3], xmax[3];
+  int32_t bc[3][2];   /* [axis][0 = low side, 1 = high side] */
+  double gamma;       /* ideal-gas gamma; e.g. 1.4 */
+  double cfl;         /* CFL number (reading c7); e.g. 0.4 */
+  double smallp;      /* pressure floor used in primitive recovery only (c10); e.g. 1e-30 */
+} orcha_grid_desc;
+
+typedef struct orcha_grid orcha_grid;
+typedef struct orcha_packet orcha_packet;
+typedef struct orcha_comm orcha_comm;
+
+/* Result of orcha_compute_dt. */
+typedef struct {
+  double dt;          /* selected time step */
+  double smax;        /* max over interior cells of the signal speed sum s */
+  int64_t argmax;     /* lowest global cell index g with s == smax */
+  int32_t tag;        /* ORCHA_DT_CFL or ORCHA_DT_CLAMP (t_end won) */
+  int32_t nonphysical;/* 1 if a non-positive/non-finite density was met */
+} orcha_dt_info;
+
+/* ------------------------------------------------------------- grid ---- */
+
+/* Validate `desc` and create a grid handle (host only, no device work).
+ * Errors: ORCHA_E_ARG (ndim, nb, nblk, extents, bc codes, gamma <= 1,
+ * cfl <= 0), ORCHA_E_HALO (ng < 4), ORCHA_E_ARG if a periodic axis has fewer
+ * cells than ng. */
+int32_t orcha_grid_create(const orcha_grid_desc* desc, orcha_grid** out);
+int32_t orcha_grid_destroy(orcha_grid* grid);
+/* Number of blocks of the global grid (NBx*NBy*NBz). */
+int64_t orcha_grid_nblocks(const orcha_grid* grid);
+
+/* ----------------------------------------------------------- packets ---- */
+
+/* Bytes of caller-owned device memory a packet of `nblocks` blocks needs:
+ * `state_bytes` for the padded conserved state (layout above) and
+ * `scratch_bytes` for the stage-1 state U1 (same padded layout; also used as
+ * the staging area of pack/unpack) plus reduction records and the status word.
+ * Host only.  Errors: ORCHA_E_ARG if nblocks < 1. */
+int32_t orcha_packet_bytes(const orcha_grid* grid, int32_t nblocks, size_t* state_bytes,
+                           size_t* scratch_bytes);
+
+/* Create a packet of `nblocks` blocks ("several blocks ... collected into a
+ * single DataPacket", sec 3.2; "n is provided by the users at
+ * runtime", sec 4.3).  `block_ids` (host, copied) gives the global
+ * block id of each slot.  d_state / d_scratch: caller-owned device memory of
+ * at least orcha_packet_bytes(), 256-byte aligned.  Allocates small
+ * library-owned device tables (per-slot block coordinates) and uploads them
+ * synchronously; no other device work.  Errors: ORCHA_E_RANGE (id outside the
+ * grid or repeated), ORCHA_E_LAYOUT (alignment), ORCHA_E_CUDA. */
+int32_t orcha_packet_create(const orcha_grid* grid, int32_t nblocks, const int64_t* block_ids,
+                            void* d_state, void* d_scratch, orcha_packet** out);
+int32_t orcha_packet_destroy(orcha_packet* packet);
+int32_t orcha_packet_nblocks(const orcha_packet* packet);
+/* Device pointer of the state and bytes of one (slot, var) cube stride. */
+int32_t orcha_packet_layout(const orcha_packet* packet, void** d_state, size_t* cube_bytes,
+                            int32_t padded_extent[3]);
+
+/* Pack: copy the packet's INTERIOR cells from host memory into the device
+ * state ("moving pointers into pinned memory and back", sec 4.3).
+ * h_interior layout: [slot][var][k][j][i] over the packet's blocks, extents
+ * nb_d (no guards), contiguous fp64.  Enqueued on `stream` (H2D into the
+ * scratch staging area, then a scatter kernel into the padded cubes); guard
+ * cells are left for orcha_fill_guardcells.  Marks the guards stale.
+ * Errors: ORCHA_E_ARG, ORCHA_E_CUDA. */
+int32_t orcha_packet_pack(orcha_packet* packet, const double* h_interior, void* stream);
+
+/* Unpack: inverse of pack (gather kernel + D2H), then synchronizes `stream`.
+ * Returns ORCHA_E_NONPHYSICAL if the packet's sticky status word recorded a
+ * non-positive or non-finite density since the last pack (data is still
+ * copied). */
+int32_t orcha_packet_unpack(const orcha_packet* packet, double* h_interior, void* stream);
+
+/* Device-to-device variants (d_interior: device pointer, same layout). */
+int32_t orcha_packet_pack_device(orcha_packet* packet, const double* d_interior, void* stream);
+int32_t orcha_packet_unpack_device(const orcha_packet* packet, double* d_interior, void* stream);
+
+/* -------------------------------------------------------- the hot path -- */
+
+/* Guard-cell fill ("We assume that the first refresh occurs before we invoke
+ * ORCHA", sec 6).  `packets` are ALL packets of
+ * this device; together (plus `comm` for blocks on other ranks, NULL on one
+ * GPU) they must hold every block the guards read.  Every guard cell of every
+ * block (faces, edges and corners, depth ng) gets the value of the global
+ * axis-ordered ghost fill (x, then y over x-guards, then z over x,y-guards):
+ * a neighbour's interior cell or the physical boundary image.  Pure copies,
+ * bitwise.  The first call with a given packet set builds and caches the
+ * neighbour tables (host + one device upload); later calls only launch.
+ * Errors: ORCHA_E_RANGE (a needed block is not resident and comm is NULL),
+ * ORCHA_E_ARG, ORCHA_E_CUDA, ORCHA_E_NCCL. */
+int32_t orcha_fill_guardcells(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
+                              void* stream);
+
+/* CFL time step over the interior cells of `packets`:
+ *   s = ((|u|+c)*idx + (|v|+c)*idy) + (|w|+c)*idz  (inactive axes omitted),
+ *   c = sqrt((gamma*p)/rho), dt = cfl / max s; argmax = lowest global g with
+ *   s == max (bitwise deterministic); then if t_remaining < dt, dt =
+ *   t_remaining (tag CLAMP).  NaN in any s propagates to dt.  With `comm`,
+ *   the max is reduced over all ranks (allreduce-max of 8 bytes).
+ * Uses the s-max records the last orcha_hydro_advance wrote for the new state
+ * when they are valid (bitwise identical to recomputing); otherwise launches
+ * the dt kernels.  Synchronizes `stream`.  Returns ORCHA_E_NONPHYSICAL if a
+ * non-positive/non-finite density was met (info still filled). */
+int32_t orcha_compute_dt(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
+                         double t_remaining, orcha_dt_info* info, void* stream);
+
+/* One full telescoped SSP-RK2 step of every block of the packet, in place
+ * (sec 6: explicit finite volume with a guard-cell halo, "2nd-order
+ * Runge-Kutta", the halo "twice as thick" so the second refresh is avoided):
+ *   stage 1 on interior + 2-cell ring:  U1 = U^n - dt*D(U^n)
+ *   stage 2 on the interior:            U^{n+1} = 0.5*(U^n + (U1 - dt*D(U1)))
+ * with D from gamma-law EOS -> PLM/minmod -> HLL.  No
+ * communication ("Milhoja only handles computations that do not involve any
+ * MPI operations").  Requires a guard fill since the last pack or
+ * advance (else ORCHA_E_STATE); marks the guards stale; writes the s-max
+ * records of U^{n+1} for orcha_compute_dt (fused dt epilogue).  Asynchronous.
+ * Non-positive densities set the sticky status word (reported by unpack /
+ * compute_dt). */
+int32_t orcha_hydro_advance(orcha_packet* packet, double dt, void* stream);
+
+/* Same, reading dt from device memory (graph-capturable: no host value). */
+int32_t orcha_hydro_advance_devdt(orcha_packet* packet, const double* d_dt, void* stream);
+
+/* ----------------------------------------------------------- support ---- */
+
+/* Counters since the last pack: pressure-floor hits in primitive recovery
+ * (reading c10) and the sticky non-physical flag with the first (lowest)
+ * offending global cell index (-1 if none).  Synchronizes `stream`. */
+int32_t orcha_packet_counters(const orcha_packet* packet, int64_t* floor_hits,
+                              int64_t* first_bad_cell, void* stream);
+
+/* Which kernel variant this library was built as: 1 = parity build (no FMA
+ * contraction, the exact expression order of SURVEY 8(c) c12; bitwise equal to
+ * the CPU oracle), 0 = production build (FMA, <= 1e-12 relative). */
+int32_t orcha_build_is_parity(void);
+
+/* Number of kernel launches this library has enqueued since load (for the
+ * bench's gpu_launches claim). */
+int64_t orcha_launch_count(void);
+
+/* Advance-kernel variant for orcha_hydro_advance: 0 = reference kernels (one
+ * thread per output cell, stencil recomputed; the structural reference),
+ * 1 = fused z-marching kernels (default; ORCHA_KERNEL=0 in the environment
+ * selects 0 at load).  Both give bitwise-identical results in the parity
+ * build.  Errors: ORCHA_E_ARG for another value. */
+int32_t orcha_set_kernel_variant(int32_t variant);
+int32_t orcha_get_kernel_variant(void);
+
+const char* orcha_last_error(void);
+
+/* ------------------------------------------------------- multi-GPU ------ */
+
+/* Communicator for blocks partitioned over ranks (one process per GPU,
+ * "4 MPI ranks, each rank talking to one GPU", sec 6.1).
+ * `block_owner[b]` (host, copied, length orcha_grid_nblocks) is the rank that
+ * owns global block b.  `nccl_unique_id` is the 128-byte ncclUniqueId that
+ * rank 0 created (orcha_comm_unique_id) and the caller broadcast (e.g. with
+ * torch.distributed).  The guard exchange is one grouped ncclSend/ncclRecv per
+ * neighbour rank of gathered guard sources; dt uses ncclAllReduce(max).
+ * Errors: ORCHA_E_ARG, ORCHA_E_NCCL. */
+int32_t orcha_comm_unique_id(void* nccl_unique_id_128);
+int32_t orcha_comm_create(const orcha_grid* grid, const void* nccl_unique_id_128, int32_t nranks,
+                          int32_t rank, const int32_t* block_owner, orcha_comm** out);
+int32_t orcha_comm_destroy(orcha_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORCHA_H */

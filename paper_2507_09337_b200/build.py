@@ -1,0 +1,80 @@
+"""Build liborcha.so (production, FMA) and liborcha_parity.so (--fmad=false,
+ORCHA_PARITY) in-tree for sm_100a with nvcc.  No JIT, no torch extension:
+the C ABI in include/orcha.h is the product boundary."""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+ROOT = os.path.dirname(HERE)
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+          "-Xptxas", "-warn-spills"]
+VARIANTS = {
+    "liborcha.so": ["--fmad=true"],
+    "liborcha_parity.so": ["--fmad=false", "-DORCHA_PARITY"],
+}
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def deps():
+    return sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(ROOT, "include", "orcha.h"), __file__]
+
+
+def _stale(target: str) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps())
+
+
+def _compile(src: str, obj: str, flags) -> str:
+    cmd = [NVCC, *ARCH, *COMMON, *flags, "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+    return r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> list:
+    out = []
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    for lib, flags in VARIANTS.items():
+        target = os.path.join(HERE, lib)
+        out.append(target)
+        if not force and not _stale(target):
+            continue
+        tag = os.path.splitext(lib)[0]
+        objs = []
+        with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+            futs = {}
+            for src in sources():
+                obj = os.path.join(objdir, f"{tag}_{os.path.splitext(os.path.basename(src))[0]}.o")
+                objs.append(obj)
+                futs[ex.submit(_compile, src, obj, flags)] = src
+            for f in cf.as_completed(futs):
+                msg = f.result()
+                if verbose and msg.strip():
+                    print(msg, file=sys.stderr)
+        tmp = target + f".{os.getpid()}.tmp"
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stderr}")
+        os.replace(tmp, target)
+    return out
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,15 @@
+// comm.h -- multi-GPU guard exchange and dt allreduce (private to liborcha.so).
+#pragma once
+#include "orcha_internal.h"
+
+namespace orcha {
+struct CommPlan;  // per fill plan: guard cells whose source block lives on another rank
+
+// Build the exchange plan for this rank's packets (host; one device upload).
+int32_t comm_build_plan(orcha_comm* comm, orcha_packet* const* pk, int npk, CommPlan** out);
+void comm_free_plan(CommPlan* plan);
+// Pack sources, exchange with every peer (grouped ncclSend/ncclRecv), unpack into guards.
+int32_t comm_exchange(orcha_comm* comm, CommPlan* plan, cudaStream_t s);
+// Global (smax, argmax) with the lowest-g tie-break and the non-physical flag.
+int32_t comm_allreduce_dt(orcha_comm* comm, double* smax, long long* g, bool* bad, cudaStream_t s);
+}  // namespace orcha

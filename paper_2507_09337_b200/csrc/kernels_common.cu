@@ -1,0 +1,158 @@
+// kernels_common.cu -- guard fill, pack/unpack, dt reduction (sm_100a, fp64).
+#include <cfloat>
+
+#include "hydro_math.cuh"
+#include "reduce.cuh"
+#include "orcha_internal.h"
+
+namespace orcha {
+
+// ------------------------------------------------------------ guard fill --
+// One thread per padded cell of every slot; interior cells return at once.
+// Guard (i,j,k) reads the neighbour-table entry of its direction and maps
+// each axis: shift (neighbour or periodic image), clamp (outflow: edge cell)
+// or mirror (reflect, negating the normal momentum) -- the per-axis images
+// compose to the global axis-ordered ghost fill.
+__global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict__ state,
+                                                   long long total, const NbrEntry* __restrict__ table) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  long long cells = (long long)G.P[0] * G.P[1] * G.P[2];
+  long long slot = t / cells;
+  long long c = t - slot * cells;
+  int pi = (int)(c % G.P[0]);
+  int pj = (int)((c / G.P[0]) % G.P[1]);
+  int pk = (int)(c / ((long long)G.P[0] * G.P[1]));
+  int l[3] = {pi - G.gd[0], pj - G.gd[1], pk - G.gd[2]};
+  int o[3];
+#pragma unroll
+  for (int d = 0; d < 3; d++) o[d] = (l[d] < 0) ? -1 : (l[d] >= G.nb[d]) ? 1 : 0;
+  if (o[0] == 0 && o[1] == 0 && o[2] == 0) return;
+  NbrEntry e = table[slot * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)];
+  if (e.src == nullptr) return;  // remote source: written by the halo exchange
+  int s[3];
+#pragma unroll
+  for (int d = 0; d < 3; d++) {
+    int m = (e.mode >> (2 * d)) & 3;
+    int n = G.nb[d];
+    if (o[d] == 0) s[d] = l[d];
+    else if (m == kShift) s[d] = l[d] - o[d] * n;
+    else if (m == kClamp) s[d] = (o[d] < 0) ? 0 : n - 1;
+    else s[d] = (o[d] < 0) ? -1 - l[d] : 2 * n - 1 - l[d];
+  }
+  long long so = cell_off(G, s[0], s[1], s[2]);
+  double* dst = state + slot * kNVar * G.cube + c;
+#pragma unroll
+  for (int v = 0; v < kNVar; v++) {
+    double x = e.src[v * G.cube + so];
+    if ((e.flip >> v) & 1) x = -x;
+    dst[v * G.cube] = x;
+  }
+}
+
+cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
+                        cudaStream_t s) {
+  long long total = (long long)nslots * G.P[0] * G.P[1] * G.P[2];
+  long long blocks = (total + 255) / 256;
+  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(G, state, total, table);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- pack / unpack --
+// staged: [slot][var][k][j][i] over nb extents (contiguous) <-> padded state.
+__global__ void __launch_bounds__(256) pack_kernel(DevGrid G, double* __restrict__ state,
+                                                   double* __restrict__ staged, long long total,
+                                                   int to_state) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  long long ncell = (long long)G.nb[0] * G.nb[1] * G.nb[2];
+  long long sv = t / ncell;  // slot*5 + var
+  long long c = t - sv * ncell;
+  int i = (int)(c % G.nb[0]);
+  int j = (int)((c / G.nb[0]) % G.nb[1]);
+  int k = (int)(c / ((long long)G.nb[0] * G.nb[1]));
+  double* p = state + sv * G.cube + cell_off(G, i, j, k);
+  if (to_state) *p = staged[t];
+  else staged[t] = *p;
+}
+
+cudaError_t launch_pack(const DevGrid& G, double* state, const double* staged, int nslots,
+                        bool to_state, cudaStream_t s) {
+  long long total = (long long)nslots * kNVar * G.nb[0] * G.nb[1] * G.nb[2];
+  long long blocks = (total + 255) / 256;
+  pack_kernel<<<(unsigned)blocks, 256, 0, s>>>(G, state, const_cast<double*>(staged), total,
+                                                to_state ? 1 : 0);
+  count_launch();
+  return cudaGetLastError();
+}
+
+__global__ void status_reset_kernel(DevStatus* st) {
+  st->first_bad = ~0ull;
+  st->floor_hits = 0ull;
+}
+
+cudaError_t launch_status_reset(DevStatus* st, cudaStream_t s) {
+  status_reset_kernel<<<1, 1, 0, s>>>(st);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Standalone CFL kernel (K4): one thread per interior cell, one record per CTA.
+template <int NDIM>
+__global__ void __launch_bounds__(256) dt_kernel(DevGrid G, const double* __restrict__ state,
+                                                 long long total, const SlotInfo* __restrict__ slots,
+                                                 DtRecord* __restrict__ rec, DevStatus* st) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double s = -DBL_MAX;
+  long long g = LLONG_MAX;
+  if (t < total) {
+    long long ncell = (long long)G.nb[0] * G.nb[1] * G.nb[2];
+    long long slot = t / ncell;
+    long long c = t - slot * ncell;
+    int i = (int)(c % G.nb[0]);
+    int j = (int)((c / G.nb[0]) % G.nb[1]);
+    int k = (int)(c / ((long long)G.nb[0] * G.nb[1]));
+    const double* p = state + slot * kNVar * G.cube + cell_off(G, i, j, k);
+    bool fl;
+    Prim q = eos(p[0], p[G.cube], p[2 * G.cube], p[3 * G.cube], p[4 * G.cube], G, &fl);
+    s = signal_speed<NDIM>(q, G);
+    SlotInfo si = slots[slot];
+    long long gi = (long long)si.bc[0] * G.nb[0] + i;
+    long long gj = (long long)si.bc[1] * G.nb[1] + j;
+    long long gk = (long long)si.bc[2] * G.nb[2] + k;
+    g = (gk * G.N[1] + gj) * G.N[0] + gi;
+    if (!(q.r > 0.0)) atomicMin(&st->first_bad, (unsigned long long)g);
+  }
+  block_reduce_rec<256>(s, g);
+  if (threadIdx.x == 0) { rec[blockIdx.x].s = s; rec[blockIdx.x].g = g; }
+}
+
+cudaError_t launch_dt(const DevGrid& G, const double* state, int nslots, const SlotInfo* slots,
+                      DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s) {
+  long long total = (long long)nslots * G.nb[0] * G.nb[1] * G.nb[2];
+  long long blocks = (total + 255) / 256;
+  if (G.ndim == 1) dt_kernel<1><<<(unsigned)blocks, 256, 0, s>>>(G, state, total, slots, records, st);
+  else if (G.ndim == 2) dt_kernel<2><<<(unsigned)blocks, 256, 0, s>>>(G, state, total, slots, records, st);
+  else dt_kernel<3><<<(unsigned)blocks, 256, 0, s>>>(G, state, total, slots, records, st);
+  count_launch();
+  *nrecords = blocks;
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(1024) dt_reduce_kernel(const DtRecord* __restrict__ rec, long long n,
+                                                         DtRecord* out) {
+  double s = -DBL_MAX;
+  long long g = LLONG_MAX;
+  for (long long t = threadIdx.x; t < n; t += blockDim.x) rec_combine(s, g, rec[t].s, rec[t].g);
+  block_reduce_rec<1024>(s, g);
+  if (threadIdx.x == 0) { out->s = s; out->g = g; }
+}
+
+cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out, cudaStream_t s) {
+  dt_reduce_kernel<<<1, 1024, 0, s>>>(records, n, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace orcha

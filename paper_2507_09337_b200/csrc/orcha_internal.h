@@ -1,0 +1,120 @@
+// orcha_internal.h -- private declarations shared by the runtime (host) and the
+// sm_100a kernels of liborcha.so.  Nothing here is part of the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/orcha.h"
+
+namespace orcha {
+
+constexpr int kNVar = 5;          // rho, rho*u, rho*v, rho*w, E (SURVEY 8 "nvar = 5 in every dimension")
+constexpr size_t kAlign = 256;    // every (slot, var) cube starts on a 256-byte boundary
+
+// Per-axis guard-source mode of a neighbour-table entry.
+enum : int { kShift = 0, kClamp = 1, kMirror = 2 };
+
+// Device-side constant description of the grid (passed by value to kernels).
+struct DevGrid {
+  int ndim;
+  int nb[3];        // cells per block per axis
+  int ng;           // guard width
+  int gd[3];        // guard width per axis (ng on active axes, 0 otherwise)
+  int P[3];         // padded extents per axis
+  int N[3];         // global cells per axis
+  int nblk[3];      // blocks per axis
+  long long cube;   // doubles between consecutive (slot, var) cubes
+  double id[3];     // 1/dx per axis (1/dx computed once)
+  double gamma, gm1, ig1, cfl, smallp;  // gm1 = gamma - 1, ig1 = 1/(gamma - 1)
+};
+
+// One entry per (slot, neighbour direction); 27 per slot, dir = (oz+1)*9 + (oy+1)*3 + (ox+1).
+struct NbrEntry {
+  const double* src;   // base of the source block's var-0 cube (nullptr = remote, filled by exchange)
+  int32_t mode;        // 2 bits per axis: kShift / kClamp / kMirror
+  int32_t flip;        // bit (1+d) set -> negate variable 1+d (reflect on axis d)
+};
+
+// Sticky per-packet status word (lives in the scratch tail).
+struct DevStatus {
+  unsigned long long first_bad;   // lowest global cell index with a non-physical state (ULLONG_MAX = none)
+  unsigned long long floor_hits;  // pressure-floor hits (own-cell primitive recovery per cell-stage)
+};
+
+// (s, g) reduction record: max s, ties -> lowest g, NaN wins (lowest g among NaN).
+struct DtRecord {
+  double s;
+  long long g;
+};
+
+struct SlotInfo {     // per slot: block coordinates (bi, bj, bk)
+  int bc[3];
+  int pad;
+};
+
+__host__ __device__ inline bool dt_better(double sa, long long ga, double sb, long long gb) {
+  bool na = sa != sa, nb = sb != sb;
+  if (na || nb) return na && (!nb || ga < gb);
+  return sa > sb || (sa == sb && ga < gb);
+}
+
+}  // namespace orcha
+
+// --------------------------------------------------------------- host side --
+struct orcha_grid {
+  orcha_grid_desc desc;
+  orcha::DevGrid dev;
+  long long nblocks;
+};
+
+struct FillPlan;  // runtime.cu
+
+struct orcha_packet {
+  const orcha_grid* grid;
+  int nslots;
+  std::vector<long long> ids;
+  double* state;               // caller-owned
+  double* scratch;             // caller-owned: U1 cubes, then tail
+  orcha::DevStatus* status;    // in scratch tail
+  orcha::DtRecord* result;     // in scratch tail (1 record)
+  orcha::DtRecord* records;    // in scratch tail
+  long long records_cap;
+  long long nrecords;          // records written by the last advance/dt kernel
+  orcha::SlotInfo* d_slots;    // library-owned device table
+  bool guards_valid;
+  bool records_valid;
+};
+
+namespace orcha {
+
+// error plumbing (runtime.cu)
+int32_t fail(int32_t code, const std::string& msg);
+int32_t cuda_fail(cudaError_t e, const char* what);
+void count_launch(long long n = 1);
+
+// layout helpers
+long long cube_doubles(const DevGrid& G);
+size_t state_bytes(const DevGrid& G, long long nslots);
+long long records_capacity(const DevGrid& G, long long nslots);
+
+// kernel launchers (kernels_*.cu); all return cudaGetLastError()
+cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
+                        cudaStream_t s);
+cudaError_t launch_pack(const DevGrid& G, double* state, const double* staged, int nslots,
+                        bool to_state, cudaStream_t s);
+cudaError_t launch_status_reset(DevStatus* st, cudaStream_t s);
+cudaError_t launch_dt(const DevGrid& G, const double* state, int nslots, const SlotInfo* slots,
+                      DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s);
+cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out, cudaStream_t s);
+cudaError_t launch_advance(const DevGrid& G, double* state, double* u1, int nslots,
+                           const SlotInfo* slots, const double* d_dt, double h_dt,
+                           DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s);
+
+// kernel variant selection (0 = reference per-cell kernels, 1 = fused z-marching)
+int kernel_variant();
+
+}  // namespace orcha

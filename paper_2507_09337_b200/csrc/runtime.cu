@@ -1,0 +1,527 @@
+// runtime.cu -- host side of liborcha.so: grid/packet bookkeeping, neighbour
+// tables, the guard-fill plan cache, dt selection and the C ABI entry points.
+//
+// Bookkeeping is bit-exact by construction (integers only): global block id
+// b = (bk*NBy + bj)*NBx + bi, slot = position in the caller's block_ids,
+// global cell g = (k*Ny + j)*Nx + i.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "comm.h"
+#include "orcha_internal.h"
+
+using namespace orcha;
+
+// ------------------------------------------------------------ errors ------
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+namespace orcha {
+int32_t fail(int32_t code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int32_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(ORCHA_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+long long cube_doubles(const DevGrid& G) {
+  long long cells = (long long)G.P[0] * G.P[1] * G.P[2];
+  long long bytes = cells * 8;
+  bytes = (bytes + (long long)kAlign - 1) / (long long)kAlign * (long long)kAlign;
+  return bytes / 8;
+}
+size_t state_bytes(const DevGrid& G, long long nslots) { return (size_t)nslots * kNVar * G.cube * 8; }
+long long records_capacity(const DevGrid& G, long long nslots) {
+  long long ncell = (long long)G.nb[0] * G.nb[1] * G.nb[2];
+  return nslots * ((ncell + 63) / 64) + 64;
+}
+
+static int g_variant = -1;
+int kernel_variant() {
+  if (g_variant < 0) {
+    const char* e = getenv("ORCHA_KERNEL");
+    g_variant = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_variant;
+}
+
+cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
+                               const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
+                               DevStatus* st, cudaStream_t s);
+cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
+                                 const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
+                                 DevStatus* st, cudaStream_t s);
+}  // namespace orcha
+
+extern "C" const char* orcha_last_error(void) { return g_last_error.c_str(); }
+extern "C" int64_t orcha_launch_count(void) { return g_launches.load(); }
+extern "C" int32_t orcha_build_is_parity(void) {
+#ifdef ORCHA_PARITY
+  return 1;
+#else
+  return 0;
+#endif
+}
+extern "C" int32_t orcha_set_kernel_variant(int32_t v) {
+  if (v < 0 || v > 1) return fail(ORCHA_E_ARG, "kernel variant must be 0 (reference) or 1 (fused)");
+  g_variant = v;
+  return ORCHA_OK;
+}
+extern "C" int32_t orcha_get_kernel_variant(void) { return kernel_variant(); }
+
+// -------------------------------------------------------------- grid ------
+extern "C" int32_t orcha_grid_create(const orcha_grid_desc* d, orcha_grid** out) {
+  if (!d || !out) return fail(ORCHA_E_ARG, "null argument");
+  *out = nullptr;
+  if (d->ndim < 1 || d->ndim > 3) return fail(ORCHA_E_ARG, "ndim must be 1, 2 or 3");
+  if (d->ng < 4) return fail(ORCHA_E_HALO, "ng < 4: the telescoped RK2 step needs a twice-thick halo (2 x PLM radius)");
+  for (int a = 0; a < 3; a++) {
+    if (a < d->ndim) {
+      if (d->nb[a] < 1 || d->nblk[a] < 1) return fail(ORCHA_E_ARG, "nb and nblk must be >= 1 on active axes");
+      if (d->nb[a] < d->ng) return fail(ORCHA_E_ARG, "nb < ng: guards would need second neighbours");
+      if (!(d->xmax[a] > d->xmin[a])) return fail(ORCHA_E_ARG, "xmax must exceed xmin");
+      for (int s = 0; s < 2; s++)
+        if (d->bc[a][s] < 0 || d->bc[a][s] > 2) return fail(ORCHA_E_ARG, "bad boundary code");
+      if ((d->bc[a][0] == ORCHA_BC_PERIODIC) != (d->bc[a][1] == ORCHA_BC_PERIODIC))
+        return fail(ORCHA_E_ARG, "periodic must be set on both sides of an axis");
+    } else if (d->nb[a] != 1 || d->nblk[a] != 1) {
+      return fail(ORCHA_E_ARG, "inactive axes must have nb = nblk = 1");
+    }
+  }
+  if (!(d->gamma > 1.0) || !(d->cfl > 0.0) || !(d->smallp >= 0.0)) return fail(ORCHA_E_ARG, "bad gamma/cfl/smallp");
+  orcha_grid* g = new orcha_grid();
+  g->desc = *d;
+  DevGrid& G = g->dev;
+  G.ndim = d->ndim;
+  G.ng = d->ng;
+  g->nblocks = 1;
+  for (int a = 0; a < 3; a++) {
+    bool act = a < d->ndim;
+    G.nb[a] = d->nb[a];
+    G.gd[a] = act ? d->ng : 0;
+    G.P[a] = d->nb[a] + 2 * G.gd[a];
+    G.nblk[a] = d->nblk[a];
+    G.N[a] = d->nb[a] * d->nblk[a];
+    double dx = act ? (d->xmax[a] - d->xmin[a]) / (double)G.N[a] : 1.0;
+    G.id[a] = act ? 1.0 / dx : 0.0;
+    g->nblocks *= d->nblk[a];
+  }
+  G.cube = cube_doubles(G);
+  G.gamma = d->gamma;
+  G.gm1 = d->gamma - 1.0;
+  G.ig1 = 1.0 / (d->gamma - 1.0);
+  G.cfl = d->cfl;
+  G.smallp = d->smallp;
+  *out = g;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_grid_destroy(orcha_grid* g) {
+  delete g;
+  return ORCHA_OK;
+}
+extern "C" int64_t orcha_grid_nblocks(const orcha_grid* g) { return g ? g->nblocks : -1; }
+
+// ------------------------------------------------------------ packets -----
+namespace {
+struct Tail {
+  size_t status_off, result_off, records_off, bytes;
+};
+Tail tail_layout(const DevGrid& G, long long nslots) {
+  Tail t;
+  t.status_off = state_bytes(G, nslots);  // the U1 cubes come first
+  t.result_off = t.status_off + 256;
+  t.records_off = t.result_off + 256;
+  t.bytes = t.records_off + (size_t)records_capacity(G, nslots) * sizeof(DtRecord);
+  t.bytes = (t.bytes + kAlign - 1) / kAlign * kAlign;
+  return t;
+}
+}  // namespace
+
+extern "C" int32_t orcha_packet_bytes(const orcha_grid* g, int32_t n, size_t* sb, size_t* xb) {
+  if (!g || n < 1) return fail(ORCHA_E_ARG, "grid null or nblocks < 1");
+  if (sb) *sb = state_bytes(g->dev, n);
+  if (xb) *xb = tail_layout(g->dev, n).bytes;
+  return ORCHA_OK;
+}
+
+struct FillPlan {
+  std::vector<orcha_packet*> packets;
+  std::vector<NbrEntry*> d_tables;   // one per packet (library-owned device memory)
+  CommPlan* remote = nullptr;        // guard cells sourced from other ranks (comm.cu)
+  bool has_remote = false;
+};
+static std::mutex g_plan_mu;
+static std::vector<FillPlan*> g_plans;
+
+static void drop_plans_with(orcha_packet* p) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (size_t i = 0; i < g_plans.size();) {
+    FillPlan* f = g_plans[i];
+    bool hit = false;
+    for (auto* q : f->packets) hit |= (q == p);
+    if (hit) {
+      for (auto* t : f->d_tables) cudaFree(t);
+      comm_free_plan(f->remote);
+      delete f;
+      g_plans.erase(g_plans.begin() + i);
+    } else {
+      i++;
+    }
+  }
+}
+
+extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int64_t* ids, void* d_state,
+                                       void* d_scratch, orcha_packet** out) {
+  if (!g || !ids || !out || n < 1) return fail(ORCHA_E_ARG, "null argument or nblocks < 1");
+  *out = nullptr;
+  if (!d_state || !d_scratch) return fail(ORCHA_E_ARG, "null device buffer");
+  if (((uintptr_t)d_state % kAlign) || ((uintptr_t)d_scratch % kAlign))
+    return fail(ORCHA_E_LAYOUT, "device buffers must be 256-byte aligned");
+  std::unordered_map<long long, int> seen;
+  for (int s = 0; s < n; s++) {
+    if (ids[s] < 0 || ids[s] >= g->nblocks) return fail(ORCHA_E_RANGE, "block id out of range (BlockOutOfRange)");
+    if (!seen.emplace(ids[s], s).second) return fail(ORCHA_E_RANGE, "duplicate block id in packet");
+  }
+  orcha_packet* p = new orcha_packet();
+  p->grid = g;
+  p->nslots = n;
+  p->ids.assign(ids, ids + n);
+  p->state = (double*)d_state;
+  p->scratch = (double*)d_scratch;
+  Tail t = tail_layout(g->dev, n);
+  char* base = (char*)d_scratch;
+  p->status = (DevStatus*)(base + t.status_off);
+  p->result = (DtRecord*)(base + t.result_off);
+  p->records = (DtRecord*)(base + t.records_off);
+  p->records_cap = records_capacity(g->dev, n);
+  p->nrecords = 0;
+  p->guards_valid = false;
+  p->records_valid = false;
+  std::vector<SlotInfo> si(n);
+  const DevGrid& G = g->dev;
+  for (int s = 0; s < n; s++) {
+    long long b = ids[s];
+    si[s].bc[0] = (int)(b % G.nblk[0]);
+    si[s].bc[1] = (int)((b / G.nblk[0]) % G.nblk[1]);
+    si[s].bc[2] = (int)(b / ((long long)G.nblk[0] * G.nblk[1]));
+    si[s].pad = 0;
+  }
+  cudaError_t e = cudaMalloc(&p->d_slots, sizeof(SlotInfo) * n);
+  if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaMalloc(slot table)"); }
+  e = cudaMemcpy(p->d_slots, si.data(), sizeof(SlotInfo) * n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(p->d_slots); delete p; return cuda_fail(e, "upload slot table"); }
+  e = launch_status_reset(p->status, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cudaFree(p->d_slots); delete p; return cuda_fail(e, "status reset"); }
+  *out = p;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_packet_destroy(orcha_packet* p) {
+  if (!p) return ORCHA_OK;
+  drop_plans_with(p);
+  cudaFree(p->d_slots);
+  delete p;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_packet_nblocks(const orcha_packet* p) { return p ? p->nslots : -1; }
+
+extern "C" int32_t orcha_packet_layout(const orcha_packet* p, void** d_state, size_t* cube_bytes,
+                                       int32_t padded_extent[3]) {
+  if (!p) return fail(ORCHA_E_ARG, "null packet");
+  if (d_state) *d_state = p->state;
+  if (cube_bytes) *cube_bytes = (size_t)p->grid->dev.cube * 8;
+  if (padded_extent)
+    for (int a = 0; a < 3; a++) padded_extent[a] = p->grid->dev.P[a];
+  return ORCHA_OK;
+}
+
+static size_t interior_bytes(const orcha_packet* p) {
+  const DevGrid& G = p->grid->dev;
+  return (size_t)p->nslots * kNVar * G.nb[0] * G.nb[1] * G.nb[2] * 8;
+}
+
+static int32_t pack_impl(orcha_packet* p, const double* src, cudaMemcpyKind kind, void* stream) {
+  if (!p || !src) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(p->scratch, src, interior_bytes(p), kind, s);
+  if (e != cudaSuccess) return cuda_fail(e, "pack copy");
+  e = launch_pack(p->grid->dev, p->state, p->scratch, p->nslots, true, s);
+  if (e == cudaSuccess) e = launch_status_reset(p->status, s);
+  if (e != cudaSuccess) return cuda_fail(e, "pack kernel");
+  p->guards_valid = false;
+  p->records_valid = false;
+  return ORCHA_OK;
+}
+
+static int32_t check_status(const orcha_packet* p, cudaStream_t s, DevStatus* out) {
+  DevStatus st;
+  cudaError_t e = cudaMemcpyAsync(&st, p->status, sizeof(st), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "read status");
+  if (out) *out = st;
+  if (st.first_bad != ~0ull) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "non-physical state (rho <= 0 or non-finite) first at global cell %llu (NonPositiveState)",
+             st.first_bad);
+    return fail(ORCHA_E_NONPHYSICAL, buf);
+  }
+  return ORCHA_OK;
+}
+
+static int32_t unpack_impl(const orcha_packet* p, double* dst, cudaMemcpyKind kind, void* stream) {
+  if (!p || !dst) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_pack(p->grid->dev, p->state, p->scratch, p->nslots, false, s);
+  if (e != cudaSuccess) return cuda_fail(e, "unpack kernel");
+  e = cudaMemcpyAsync(dst, p->scratch, interior_bytes(p), kind, s);
+  if (e != cudaSuccess) return cuda_fail(e, "unpack copy");
+  return check_status(p, s, nullptr);
+}
+
+extern "C" int32_t orcha_packet_pack(orcha_packet* p, const double* h, void* stream) {
+  return pack_impl(p, h, cudaMemcpyHostToDevice, stream);
+}
+extern "C" int32_t orcha_packet_pack_device(orcha_packet* p, const double* d, void* stream) {
+  return pack_impl(p, d, cudaMemcpyDeviceToDevice, stream);
+}
+extern "C" int32_t orcha_packet_unpack(const orcha_packet* p, double* h, void* stream) {
+  return unpack_impl(p, h, cudaMemcpyDeviceToHost, stream);
+}
+extern "C" int32_t orcha_packet_unpack_device(const orcha_packet* p, double* d, void* stream) {
+  return unpack_impl(p, d, cudaMemcpyDeviceToDevice, stream);
+}
+
+extern "C" int32_t orcha_packet_counters(const orcha_packet* p, int64_t* floor_hits, int64_t* first_bad,
+                                         void* stream) {
+  if (!p) return fail(ORCHA_E_ARG, "null packet");
+  DevStatus st;
+  int32_t rc = check_status(p, (cudaStream_t)stream, &st);
+  if (rc == ORCHA_E_CUDA) return rc;
+  if (floor_hits) *floor_hits = (int64_t)st.floor_hits;
+  if (first_bad) *first_bad = st.first_bad == ~0ull ? -1 : (int64_t)st.first_bad;
+  return ORCHA_OK;
+}
+
+// -------------------------------------------------------- guard fill -----
+// Neighbour-table entry for (block coords bc, direction o): per axis either
+// stay (o=0), step to the neighbour (inside, or periodic wrap), clamp
+// (outflow) or mirror (reflect, flip the normal momentum).
+struct HostEntry {
+  long long src_block;
+  int mode, flip;
+};
+static HostEntry make_entry(const orcha_grid* g, const int bc[3], const int o[3]) {
+  const DevGrid& G = g->dev;
+  HostEntry h{0, 0, 0};
+  int nb3[3];
+  for (int a = 0; a < 3; a++) {
+    int m = kShift;
+    int c = bc[a] + o[a];
+    if (o[a] != 0 && (c < 0 || c >= G.nblk[a])) {
+      int code = g->desc.bc[a][o[a] < 0 ? 0 : 1];
+      if (code == ORCHA_BC_PERIODIC) {
+        c = (c + G.nblk[a]) % G.nblk[a];
+      } else if (code == ORCHA_BC_OUTFLOW) {
+        c = bc[a];
+        m = kClamp;
+      } else {
+        c = bc[a];
+        m = kMirror;
+        h.flip |= 1 << (1 + a);
+      }
+    }
+    nb3[a] = c;
+    h.mode |= m << (2 * a);
+  }
+  h.src_block = ((long long)nb3[2] * G.nblk[1] + nb3[1]) * G.nblk[0] + nb3[0];
+  return h;
+}
+
+static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, FillPlan** out) {
+  const orcha_grid* g = pk[0]->grid;
+  const DevGrid& G = g->dev;
+  std::unordered_map<long long, std::pair<int, int>> where;  // block -> (packet, slot)
+  for (int q = 0; q < npk; q++) {
+    if (pk[q]->grid != g) return fail(ORCHA_E_ARG, "packets belong to different grids");
+    for (int s = 0; s < pk[q]->nslots; s++)
+      if (!where.emplace(pk[q]->ids[s], std::make_pair(q, s)).second)
+        return fail(ORCHA_E_RANGE, "block resident in two packets");
+  }
+  FillPlan* f = new FillPlan();
+  f->packets.assign(pk, pk + npk);
+  for (int q = 0; q < npk; q++) {
+    orcha_packet* p = pk[q];
+    std::vector<NbrEntry> tab((size_t)p->nslots * 27);
+    for (int s = 0; s < p->nslots; s++) {
+      long long b = p->ids[s];
+      int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
+                   (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+      for (int oz = -1; oz <= 1; oz++)
+        for (int oy = -1; oy <= 1; oy++)
+          for (int ox = -1; ox <= 1; ox++) {
+            int o[3] = {ox, oy, oz};
+            NbrEntry& e = tab[(size_t)s * 27 + (oz + 1) * 9 + (oy + 1) * 3 + (ox + 1)];
+            bool valid = true;
+            for (int a = g->desc.ndim; a < 3; a++) valid &= (o[a] == 0);
+            if (!valid) { e.src = p->state; e.mode = 0; e.flip = 0; continue; }
+            HostEntry h = make_entry(g, bc, o);
+            e.mode = h.mode;
+            e.flip = h.flip;
+            auto it = where.find(h.src_block);
+            if (it == where.end()) {
+              if (!comm) {
+                for (auto* t : f->d_tables) cudaFree(t);
+                delete f;
+                return fail(ORCHA_E_RANGE, "neighbour block " + std::to_string(h.src_block) +
+                                               " is not resident on this device and no communicator was given");
+              }
+              e.src = nullptr;
+              f->has_remote = true;
+            } else {
+              orcha_packet* sp = pk[it->second.first];
+              e.src = sp->state + (long long)it->second.second * kNVar * G.cube;
+            }
+          }
+    }
+    NbrEntry* d = nullptr;
+    cudaError_t err = cudaMalloc(&d, tab.size() * sizeof(NbrEntry));
+    if (err == cudaSuccess) err = cudaMemcpy(d, tab.data(), tab.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) {
+      for (auto* t : f->d_tables) cudaFree(t);
+      delete f;
+      return cuda_fail(err, "upload neighbour table");
+    }
+    f->d_tables.push_back(d);
+  }
+  if (f->has_remote) {
+    int32_t rc = comm_build_plan(comm, pk, npk, &f->remote);
+    if (rc) {
+      for (auto* t : f->d_tables) cudaFree(t);
+      delete f;
+      return rc;
+    }
+  }
+  *out = f;
+  return ORCHA_OK;
+}
+
+static int32_t get_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, FillPlan** out) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (auto* f : g_plans) {
+    if ((int)f->packets.size() != npk) continue;
+    bool same = true;
+    for (int q = 0; q < npk; q++) same &= f->packets[q] == pk[q];
+    if (same && (!f->has_remote || comm)) { *out = f; return ORCHA_OK; }
+  }
+  FillPlan* f = nullptr;
+  int32_t rc = build_plan(pk, npk, comm, &f);
+  if (rc) return rc;
+  g_plans.push_back(f);
+  *out = f;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_fill_guardcells(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, void* stream) {
+  if (!pk || npk < 1) return fail(ORCHA_E_ARG, "no packets");
+  for (int q = 0; q < npk; q++)
+    if (!pk[q]) return fail(ORCHA_E_ARG, "null packet");
+  FillPlan* f = nullptr;
+  int32_t rc = get_plan(pk, npk, comm, &f);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (f->has_remote) {
+    rc = comm_exchange(comm, f->remote, s);
+    if (rc) return rc;
+  }
+  for (int q = 0; q < npk; q++) {
+    cudaError_t e = launch_fill(pk[q]->grid->dev, pk[q]->state, pk[q]->nslots, f->d_tables[q], s);
+    if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
+  }
+  for (int q = 0; q < npk; q++) pk[q]->guards_valid = true;
+  return ORCHA_OK;
+}
+
+// --------------------------------------------------------------- dt ------
+extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, double t_remaining,
+                                    orcha_dt_info* info, void* stream) {
+  if (!pk || npk < 1 || !info) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<DtRecord> res(npk);
+  std::vector<DevStatus> st(npk);
+  for (int q = 0; q < npk; q++) {
+    orcha_packet* p = pk[q];
+    if (!p) return fail(ORCHA_E_ARG, "null packet");
+    cudaError_t e = cudaSuccess;
+    if (!p->records_valid) {
+      e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords, p->status, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dt kernel");
+      p->records_valid = true;
+    }
+    e = launch_dt_reduce(p->records, p->nrecords, p->result, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&res[q], p->result, sizeof(DtRecord), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&st[q], p->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt reduce");
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "dt sync");
+  double smax = res[0].s;
+  long long g = res[0].g;
+  bool bad = false;
+  for (int q = 0; q < npk; q++) {
+    if (dt_better(res[q].s, res[q].g, smax, g)) { smax = res[q].s; g = res[q].g; }
+    bad |= st[q].first_bad != ~0ull;
+  }
+  if (comm) {
+    int32_t rc = comm_allreduce_dt(comm, &smax, &g, &bad, s);
+    if (rc) return rc;
+  }
+  const double cfl = pk[0]->grid->dev.cfl;
+  double dt = cfl / smax;
+  int32_t tag = ORCHA_DT_CFL;
+  if (t_remaining < dt) { dt = t_remaining; tag = ORCHA_DT_CLAMP; }
+  info->dt = dt;
+  info->smax = smax;
+  info->argmax = g;
+  info->tag = tag;
+  info->nonphysical = bad ? 1 : 0;
+  if (bad) return fail(ORCHA_E_NONPHYSICAL, "non-physical state (rho <= 0 or non-finite) in a packet (NonPositiveState)");
+  return ORCHA_OK;
+}
+
+// ----------------------------------------------------------- advance -----
+static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, void* stream) {
+  if (!p) return fail(ORCHA_E_ARG, "null packet");
+  if (!p->guards_valid)
+    return fail(ORCHA_E_STATE, "orcha_fill_guardcells must precede every orcha_hydro_advance (guards are stale)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevGrid& G = p->grid->dev;
+  cudaError_t e;
+  if (kernel_variant() == 0)
+    e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
+                           p->status, s);
+  else
+    e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
+                             &p->nrecords, p->status, s);
+  if (e != cudaSuccess) return cuda_fail(e, "advance kernels");
+  if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
+  p->guards_valid = false;
+  p->records_valid = true;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_hydro_advance(orcha_packet* p, double dt, void* stream) {
+  return advance_impl(p, nullptr, dt, stream);
+}
+extern "C" int32_t orcha_hydro_advance_devdt(orcha_packet* p, const double* d_dt, void* stream) {
+  if (!d_dt) return fail(ORCHA_E_ARG, "null d_dt");
+  return advance_impl(p, d_dt, 0.0, stream);
+}

@@ -1,0 +1,188 @@
+"""Thin Python objects over the C ABI (include/orcha.h).
+
+PyTorch supplies only device memory (caller-owned buffers handed to the
+library as raw pointers) and streams; every step of the hot path runs in the
+library's kernels.  Function names mirror the C entry points.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import abi
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Grid:
+    """A global grid of nblk blocks of nb cells with ng guard cells."""
+
+    def __init__(self, ndim: int, nb: Sequence[int], nblk: Sequence[int], ng: int = 4,
+                 xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), bc=((0, 0), (0, 0), (0, 0)),
+                 gamma: float = 1.4, cfl: float = 0.4, smallp: float = 1e-30, parity: bool = False):
+        self.lib = abi.load(parity)
+        self.parity = parity
+        nb = list(nb) + [1] * (3 - len(nb))
+        nblk = list(nblk) + [1] * (3 - len(nblk))
+        d = abi.orcha_grid_desc()
+        d.ndim = ndim
+        for a in range(3):
+            d.nb[a] = int(nb[a])
+            d.nblk[a] = int(nblk[a])
+            d.xmin[a] = float(xmin[a]) if a < len(xmin) else 0.0
+            d.xmax[a] = float(xmax[a]) if a < len(xmax) else 1.0
+            d.bc[a][0] = int(bc[a][0])
+            d.bc[a][1] = int(bc[a][1])
+        d.ng = ng
+        d.gamma, d.cfl, d.smallp = gamma, cfl, smallp
+        self.desc = d
+        self.ndim, self.nb, self.nblk, self.ng = ndim, tuple(nb), tuple(nblk), ng
+        self.N = tuple(nb[a] * nblk[a] for a in range(3))
+        h = ctypes.c_void_p()
+        abi.call(self.lib, "orcha_grid_create", ctypes.byref(d), ctypes.byref(h))
+        self.handle = h
+        self.nblocks = int(self.lib.orcha_grid_nblocks(h))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            self.lib.orcha_grid_destroy(self.handle)
+            self.handle = None
+
+    def packet_bytes(self, nblocks: int):
+        sb, xb = ctypes.c_size_t(), ctypes.c_size_t()
+        abi.call(self.lib, "orcha_packet_bytes", self.handle, nblocks, ctypes.byref(sb), ctypes.byref(xb))
+        return sb.value, xb.value
+
+
+class Packet:
+    """N blocks of the grid in caller-owned device memory (torch tensors)."""
+
+    def __init__(self, grid: Grid, block_ids: Sequence[int], device="cuda"):
+        self.grid = grid
+        self.lib = grid.lib
+        self.block_ids = np.ascontiguousarray(block_ids, dtype=np.int64)
+        n = len(self.block_ids)
+        sb, xb = grid.packet_bytes(n)
+        self.state = torch.empty(sb, dtype=torch.uint8, device=device)
+        self.scratch = torch.empty(xb, dtype=torch.uint8, device=device)
+        h = ctypes.c_void_p()
+        abi.call(self.lib, "orcha_packet_create", grid.handle, n,
+                 self.block_ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                 ctypes.c_void_p(self.state.data_ptr()), ctypes.c_void_p(self.scratch.data_ptr()),
+                 ctypes.byref(h))
+        self.handle = h
+        self.nblocks = n
+        cb = ctypes.c_size_t()
+        ext = (ctypes.c_int32 * 3)()
+        abi.call(self.lib, "orcha_packet_layout", h, None, ctypes.byref(cb), ext)
+        self.cube_doubles = cb.value // 8
+        self.padded = tuple(ext)
+        self.interior_shape = (n, 5, grid.nb[2], grid.nb[1], grid.nb[0])
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            self.lib.orcha_packet_destroy(self.handle)
+            self.handle = None
+
+    # --- pack / unpack (packet moved as one flattened buffer) ---
+    def pack(self, interior, stream=None):
+        """interior: (nblocks, 5, nbz, nby, nbx) float64, numpy (host) or torch (host or device)."""
+        if isinstance(interior, np.ndarray):
+            a = np.ascontiguousarray(interior, dtype=np.float64)
+            assert a.shape == self.interior_shape, (a.shape, self.interior_shape)
+            abi.call(self.lib, "orcha_packet_pack", self.handle, ctypes.c_void_p(a.ctypes.data),
+                     ctypes.c_void_p(_stream_ptr(stream)))
+            torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+            return
+        t = interior
+        assert t.dtype == torch.float64 and t.is_contiguous() and tuple(t.shape) == self.interior_shape
+        name = "orcha_packet_pack_device" if t.is_cuda else "orcha_packet_pack"
+        abi.call(self.lib, name, self.handle, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(_stream_ptr(stream)))
+
+    def unpack(self, out=None, stream=None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.interior_shape, dtype=np.float64)
+        if isinstance(out, np.ndarray):
+            abi.call(self.lib, "orcha_packet_unpack", self.handle, ctypes.c_void_p(out.ctypes.data),
+                     ctypes.c_void_p(_stream_ptr(stream)))
+            return out
+        name = "orcha_packet_unpack_device" if out.is_cuda else "orcha_packet_unpack"
+        abi.call(self.lib, name, self.handle, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream)))
+        return out
+
+    def state_view(self) -> torch.Tensor:
+        """(nblocks, 5, Pz, Py, Px) float64 view of the padded state incl. guards."""
+        P = self.padded
+        cells = P[0] * P[1] * P[2]
+        v = self.state.view(torch.float64).view(self.nblocks, 5, self.cube_doubles)[:, :, :cells]
+        return v.reshape(self.nblocks, 5, P[2], P[1], P[0])
+
+    def counters(self, stream=None):
+        fh, fb = ctypes.c_int64(), ctypes.c_int64()
+        abi.call(self.lib, "orcha_packet_counters", self.handle, ctypes.byref(fh), ctypes.byref(fb),
+                 ctypes.c_void_p(_stream_ptr(stream)))
+        return fh.value, fb.value
+
+
+def _handles(packets):
+    arr = (ctypes.c_void_p * len(packets))(*[p.handle.value for p in packets])
+    return arr, len(packets)
+
+
+def orcha_fill_guardcells(packets, comm=None, stream=None):
+    arr, n = _handles(packets)
+    lib = packets[0].lib
+    abi.call(lib, "orcha_fill_guardcells", arr, n, comm.handle if comm is not None else None,
+             ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def orcha_compute_dt(packets, t_remaining: float = math.inf, comm=None, stream=None, check: bool = True):
+    arr, n = _handles(packets)
+    lib = packets[0].lib
+    info = abi.orcha_dt_info()
+    rc = lib.orcha_compute_dt(arr, n, comm.handle if comm is not None else None, float(t_remaining),
+                              ctypes.byref(info), ctypes.c_void_p(_stream_ptr(stream)))
+    if check:
+        abi.check(lib, rc, "orcha_compute_dt")
+    return info
+
+
+def orcha_hydro_advance(packet: Packet, dt: float, stream=None):
+    abi.call(packet.lib, "orcha_hydro_advance", packet.handle, float(dt), ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def orcha_hydro_advance_devdt(packet: Packet, d_dt: torch.Tensor, stream=None):
+    assert d_dt.dtype == torch.float64 and d_dt.is_cuda
+    abi.call(packet.lib, "orcha_hydro_advance_devdt", packet.handle, ctypes.c_void_p(d_dt.data_ptr()),
+             ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def set_kernel_variant(lib, v: int):
+    abi.call(lib, "orcha_set_kernel_variant", int(v))
+
+
+def run(packets, nsteps: Optional[int] = None, t_end: float = math.inf, comm=None, stream=None):
+    """The driver loop of SURVEY 8(c): fill -> dt (then t_end clamp) -> advance,
+    every call through the C ABI.  Returns (t, steps, [dt_info...])."""
+    t = 0.0
+    log = []
+    n = 0
+    while (nsteps is None or n < nsteps) and t < t_end:
+        orcha_fill_guardcells(packets, comm, stream)
+        info = orcha_compute_dt(packets, t_end - t, comm, stream)
+        for p in packets:
+            orcha_hydro_advance(p, info.dt, stream)
+        t = t + info.dt
+        n += 1
+        log.append((info.dt, info.smax, info.argmax, info.tag))
+    return t, n, log

@@ -1,0 +1,93 @@
+"""Helpers for the GPU parity tests: run a global problem through the C ABI
+(packets of blocks) and compare with the oracle's global array."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+import oracle
+import orcha_inputs as inp
+
+
+def make_grid(ndim, nb, nblk, bc=None, xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), parity=False):
+    from paper_2507_09337_b200 import hydro
+    bc = bc or ((0, 0),) * 3
+    return hydro.Grid(ndim, nb, nblk, bc=bc, xmin=xmin, xmax=xmax, parity=parity)
+
+
+def oracle_grid(g) -> oracle.Grid:
+    nd = g.ndim
+    return oracle.Grid(N=tuple(g.N[:nd]), xmin=tuple(g.desc.xmin[:nd]) + (0.0,) * (3 - nd),
+                       xmax=tuple(g.desc.xmax[:nd]) + (1.0,) * (3 - nd),
+                       bc=tuple((g.desc.bc[a][0], g.desc.bc[a][1]) for a in range(3)))
+
+
+def split_packets(nblocks: int, npackets: int, seed: int = 0, shuffle: bool = False):
+    ids = np.arange(nblocks, dtype=np.int64)
+    if shuffle:
+        np.random.default_rng(seed).shuffle(ids)
+    return [a for a in np.array_split(ids, npackets) if len(a)]
+
+
+def gpu_setup(g, U0, npackets=1, shuffle=False):
+    from paper_2507_09337_b200 import hydro
+    nd = g.ndim
+    parts = split_packets(g.nblocks, npackets, shuffle=shuffle)
+    pk = [hydro.Packet(g, ids) for ids in parts]
+    for p in pk:
+        p.pack(inp.to_blocks(U0, g.nb[:nd], p.block_ids))
+    return pk
+
+
+def gather(g, pk):
+    nd = g.ndim
+    out = None
+    for p in pk:
+        out = inp.from_blocks(p.unpack(), g.N[:nd], g.nb[:nd], p.block_ids, out)
+    return out
+
+
+def gpu_run(g, U0, nsteps=None, t_end=math.inf, npackets=1, shuffle=False):
+    from paper_2507_09337_b200 import hydro
+    pk = gpu_setup(g, U0, npackets, shuffle)
+    t, n, log = hydro.run(pk, nsteps=nsteps, t_end=t_end)
+    return gather(g, pk), t, log, pk
+
+
+def oracle_run(og, U0, nsteps=None, t_end=math.inf):
+    U = oracle.padded(og, U0)
+    log = oracle.run(og, U, nsteps=nsteps, t_end=t_end)
+    return U[og.interior].copy(), log
+
+
+def parity_error(gpu: np.ndarray, ora: np.ndarray, tau_rel: float = 1e-2) -> float:
+    """Production-build metric (reading c13): max over cells and
+    variables of |g-o| / max(|o|, tau_v) with tau_v = tau_rel * max|o_v|, and
+    the per-variable ||g-o||_inf / ||o||_inf; the max of both."""
+    worst = 0.0
+    for v in range(5):
+        o = ora[v]
+        d = np.abs(gpu[v] - o)
+        omax = np.abs(o).max()
+        if omax == 0.0:
+            worst = max(worst, float(d.max()) and math.inf)
+            continue
+        tau = tau_rel * omax
+        worst = max(worst, float((d / np.maximum(np.abs(o), tau)).max()), float(d.max() / omax))
+    return worst
+
+
+def error_report(gpu: np.ndarray, ora: np.ndarray) -> dict:
+    """Per variable: ||g-o||_inf/||o||_inf and the per-cell relative error at tau 1e-6 / 1e-2."""
+    rep = {}
+    for v in range(5):
+        o = ora[v]
+        d = np.abs(gpu[v] - o)
+        omax = np.abs(o).max()
+        if omax == 0.0:
+            rep[v] = (float(d.max()), None, None)
+            continue
+        rep[v] = (float(d.max() / omax), float((d / np.maximum(np.abs(o), 1e-6 * omax)).max()),
+                  float((d / np.maximum(np.abs(o), 1e-2 * omax)).max()))
+    return rep

@@ -1,0 +1,117 @@
+"""C-ABI library checks that need no GPU: the libraries load, export every
+symbol include/orcha.h declares, and the host-only calls (descriptor
+validation, layout arithmetic) behave as documented."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2507_09337_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "orcha.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(orcha_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module", params=[False, True], ids=["production", "parity"])
+def lib(request):
+    from paper_2507_09337_b200 import build
+    build.build()
+    return abi.load(request.param)
+
+
+def test_exports_every_declared_symbol(lib):
+    names = header_functions()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(abi.EXPORTS)
+
+
+def test_build_flavour(lib):
+    path = lib._name
+    assert lib.orcha_build_is_parity() == (1 if path.endswith("_parity.so") else 0)
+
+
+def desc(ndim=3, nb=(16, 16, 16), nblk=(2, 2, 2), ng=4):
+    d = abi.orcha_grid_desc()
+    d.ndim = ndim
+    for a in range(3):
+        d.nb[a] = nb[a] if a < ndim else 1
+        d.nblk[a] = nblk[a] if a < ndim else 1
+        d.xmin[a] = 0.0
+        d.xmax[a] = 1.0
+    d.ng = ng
+    d.gamma, d.cfl, d.smallp = 1.4, 0.4, 1e-30
+    return d
+
+
+def create(lib, d):
+    h = ctypes.c_void_p()
+    rc = lib.orcha_grid_create(ctypes.byref(d), ctypes.byref(h))
+    return rc, h
+
+
+def test_grid_validation(lib):
+    rc, h = create(lib, desc())
+    assert rc == 0 and h.value
+    assert lib.orcha_grid_nblocks(h) == 8
+    lib.orcha_grid_destroy(h)
+    rc, _ = create(lib, desc(ng=2))                  # SPEC HaloTooThin
+    assert rc == -3 and b"halo" in lib.orcha_last_error()
+    rc, _ = create(lib, desc(ndim=4))
+    assert rc == -1
+    d = desc()
+    d.bc[0][0] = 1                                    # periodic on one side only
+    assert create(lib, d)[0] == -1
+    d = desc()
+    d.gamma = 1.0
+    assert create(lib, d)[0] == -1
+    d = desc(nb=(2, 16, 16))                          # block narrower than the halo
+    assert create(lib, d)[0] == -1
+    d = desc(ndim=2)
+    d.nb[2] = 4                                       # inactive axis must be 1
+    assert create(lib, d)[0] == -1
+
+
+@pytest.mark.parametrize("ndim,nb,cube_bytes", [(3, (16, 16, 16), 24 ** 3 * 8), (2, (8, 8, 1), 16 * 16 * 8),
+                                                (3, (8, 8, 8), 16 ** 3 * 8), (1, (16, 1, 1), 256),
+                                                (3, (32, 32, 32), 40 ** 3 * 8)])
+def test_packet_bytes_layout(lib, ndim, nb, cube_bytes):
+    # cubes [slot][var][k][j][i], padded n+2ng, each 256-B aligned
+    rc, g = create(lib, desc(ndim=ndim, nb=nb))
+    assert rc == 0
+    sb, xb = ctypes.c_size_t(), ctypes.c_size_t()
+    for n in (1, 7, 512):
+        assert lib.orcha_packet_bytes(g, n, ctypes.byref(sb), ctypes.byref(xb)) == 0
+        assert sb.value == n * 5 * cube_bytes
+        assert sb.value % 256 == 0 and xb.value % 256 == 0
+        assert xb.value >= sb.value          # U1 scratch has the state's layout + tail
+    assert lib.orcha_packet_bytes(g, 0, ctypes.byref(sb), ctypes.byref(xb)) == -1
+    lib.orcha_grid_destroy(g)
+
+
+def test_packet_create_rejects_bad_ids_without_device_work(lib):
+    rc, g = create(lib, desc())
+    ids = (ctypes.c_int64 * 3)(0, 1, 8)               # 8 is out of range (BlockOutOfRange)
+    h = ctypes.c_void_p()
+    fake = ctypes.c_void_p(256 * 1024)
+    assert lib.orcha_packet_create(g, 3, ids, fake, fake, ctypes.byref(h)) == -2
+    ids = (ctypes.c_int64 * 2)(3, 3)
+    assert lib.orcha_packet_create(g, 2, ids, fake, fake, ctypes.byref(h)) == -2
+    ids = (ctypes.c_int64 * 1)(0)
+    assert lib.orcha_packet_create(g, 1, ids, ctypes.c_void_p(256 * 1024 + 8), fake, ctypes.byref(h)) == -5
+    lib.orcha_grid_destroy(g)
+
+
+def test_advance_requires_fill_is_documented():
+    # the ABI invariant (hydro_advance performs no communication, fill must
+    # precede it) is stated in the header next to the entry point
+    src = open(HEADER).read()
+    assert "ORCHA_E_STATE" in src and "P:L674" in src

@@ -1,8 +1,8 @@
 mkdir -p gpurun_out
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
-lscpu | grep -E "Model name|^CPU\(s\)"
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -40 > gpurun_out/pytest_gpu.txt
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1
-timeout 600 python bench.py --steps 5 --warmup 3 --e2e-steps 1 > gpurun_out/bench.txt 2>&1
-tail -5 gpurun_out/pytest_gpu.txt; tail -3 gpurun_out/smoke.txt; tail -3 gpurun_out/bench.txt
+timeout 600 python bench.py --steps 10 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/bench.txt 2>&1
+timeout 600 python bench.py --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline --variant 0 > gpurun_out/bench_ref.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 20 -c 40 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_bench.txt 2>&1
+tail -5 gpurun_out/pytest_gpu.txt; tail -2 gpurun_out/smoke.txt; tail -2 gpurun_out/bench.txt | cut -c1-600; tail -1 gpurun_out/bench_ref.txt | cut -c1-300

@@ -233,9 +233,7 @@ def main():
         comm = hydro.Comm.create(g, world, rank, hydro.brick_owner(nblk, BRICK_BLOCKS, GPU_GRIDS[world]))
     pk = hydro.Packet(g, ids)
     # initial Sedov state of this brick (host, closed form) -> pinned -> pack
-    U0 = inp.sedov(N, xmax=(float(px), float(py), float(pz)))
-    host = torch.from_numpy(inp.to_blocks(U0, NB, ids)).pin_memory()
-    del U0
+    host = torch.from_numpy(inp.sedov_packet(N, NB, ids, xmax=(float(px), float(py), float(pz)))).pin_memory()
     stream = torch.cuda.current_stream()
     pk.pack(host, stream)
     stream.synchronize()

@@ -233,6 +233,31 @@ int32_t orcha_comm_create(const orcha_grid* grid, const void* nccl_unique_id_128
                           int32_t rank, const int32_t* block_owner, orcha_comm** out);
 int32_t orcha_comm_destroy(orcha_comm* comm);
 
+/* In-process transport for tests and single-GPU decomposition studies:
+ * creates `nranks` communicators (out[r] for virtual rank r) that share one
+ * device; their exchange is device-to-device copies instead of NCCL.  The
+ * caller first calls orcha_comm_push for EVERY virtual rank (each packs its
+ * guard sources straight into its peers' receive buffers) and then
+ * orcha_fill_guardcells for each (which unpacks and fills).  No NCCL needed. */
+int32_t orcha_comm_create_local(const orcha_grid* grid, int32_t nranks, const int32_t* block_owner,
+                                orcha_comm** out);
+int32_t orcha_comm_push(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, void* stream);
+
+/* Host-only view of the guard exchange plan between `rank` and `peer` (no
+ * device work; for tests and tooling).  The plan is a pure function of the
+ * grid and block_owner: the cells rank SENDS to peer are the sorted unique
+ * global cell indices g of its interior cells that peer's guards read; the
+ * cells it RECEIVES from peer are the same list computed on the other side;
+ * each remote guard of `rank` then takes value recv[idx] (negated in the
+ * momentum components set in flip, reflect boundaries).
+ * which: 0 = send cells (int64 g), 1 = receive cells (int64 g),
+ *        2 = receiving guards (int64: dst block id * P^3 + padded cell index),
+ *        3 = index into the receive cells (int64), 4 = flip bits (int64).
+ * out may be NULL to query *count; otherwise up to cap entries are written.
+ * Errors: ORCHA_E_ARG, ORCHA_E_RANGE (owner out of range). */
+int32_t orcha_comm_plan(const orcha_grid* grid, int32_t nranks, int32_t rank, const int32_t* block_owner,
+                        int32_t peer, int32_t which, int64_t* out, int64_t cap, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,6 +72,55 @@ def sedov(N: Sequence[int], xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), gamma: f
     return U
 
 
+def sedov_packet(N: Sequence[int], nb: Sequence[int], block_ids: Sequence[int], xmin=(0.0, 0.0, 0.0),
+                 xmax=(1.0, 1.0, 1.0), gamma: float = 1.4, E_blast: float = 1.0, p_amb: float = 1e-5,
+                 rho0: float = 1.0) -> np.ndarray:
+    """The Sedov initial state restricted to the given blocks, directly in packet
+    interior order (nblocks, 5, nbz, nby, nbx): bitwise equal to
+    to_blocks(sedov(N, ...), nb, block_ids) without building the global array
+    (a rank of the weak-scaling run only materialises its own brick)."""
+    nd = len(N)
+    Nx, Ny, Nz = _dims(N)
+    bx, by, bz = _dims(nb)
+    NBx, NBy = Nx // bx, Ny // by
+    dx = [(xmax[d] - xmin[d]) / N[d] for d in range(nd)]
+    dV = dx[0]
+    for d in range(1, nd):
+        dV = dV * dx[d]
+    # deposit cells lie within 4 cells of the centre vertex on every axis
+    lo = [n // 2 - 4 for n in (Nx, Ny, Nz)[:nd]]
+    sub = [min(8, n) for n in (Nx, Ny, Nz)[:nd]]
+    r2 = np.zeros([1, 1, 1][: 3 - nd] + list(reversed(sub)), dtype=np.int64)
+    axes_len = list(reversed(sub))
+    for d in range(nd):
+        n = (Nx, Ny, Nz)[d]
+        a = (2 * (np.arange(sub[d], dtype=np.int64) + lo[d]) + 1 - n) ** 2
+        shape = [1, 1, 1]
+        shape[2 - d] = sub[d]
+        r2 = r2 + a.reshape(shape)
+    for n in N:
+        if n % 2:
+            raise ValueError("Sedov deposit needs even N on every active axis")
+    full = np.argwhere(r2.reshape([1] * (3 - len(axes_len)) + axes_len) < 49)
+    nD = len(full)
+    ids = np.asarray(block_ids, dtype=np.int64)
+    out = np.empty((len(ids), 5, bz, by, bx), dtype=np.float64)
+    out[:, 0] = rho0
+    out[:, 1:4] = 0.0
+    out[:, 4] = p_amb * (1.0 / (gamma - 1.0))
+    slot_of = {int(b): s for s, b in enumerate(ids)}
+    Edep = E_blast / (nD * dV)
+    for kz, jy, ix in full:
+        gi = ix + lo[0]
+        gj = (jy + lo[1]) if nd > 1 else 0
+        gk = (kz + lo[2]) if nd > 2 else 0
+        b = ((gk // bz) * NBy + gj // by) * NBx + gi // bx
+        s = slot_of.get(int(b))
+        if s is not None:
+            out[s, 4, gk % bz, gj % by, gi % bx] = Edep
+    return out
+
+
 def sedov_deposit_count(ndim: int) -> int:
     """n_D for any even N >= 8: 32 in 2D, 160 in 3D (12 in 1D)."""
     return int(sedov_deposit_mask([8] * ndim).sum())

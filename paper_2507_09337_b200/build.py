@@ -14,8 +14,20 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_include() -> str:
+    """nccl.h of the NCCL torch ships (types only: the library dlopens libnccl.so.2 at run time)."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return d
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-          "-Xptxas", "-warn-spills"]
+          "-I", _nccl_include(), "-Xptxas", "-warn-spills"]
 VARIANTS = {
     "liborcha.so": ["--fmad=true"],
     "liborcha_parity.so": ["--fmad=false", "-DORCHA_PARITY"],

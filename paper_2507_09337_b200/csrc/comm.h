@@ -8,6 +8,8 @@ struct CommPlan;  // per fill plan: guard cells whose source block lives on anot
 // Build the exchange plan for this rank's packets (host; one device upload).
 int32_t comm_build_plan(orcha_comm* comm, orcha_packet* const* pk, int npk, CommPlan** out);
 void comm_free_plan(CommPlan* plan);
+// Forget cached plans that reference a packet being destroyed.
+void comm_drop_packet(orcha_packet* p);
 // Pack sources, exchange with every peer (grouped ncclSend/ncclRecv), unpack into guards.
 int32_t comm_exchange(orcha_comm* comm, CommPlan* plan, cudaStream_t s);
 // Global (smax, argmax) with the lowest-g tie-break and the non-physical flag.

@@ -227,6 +227,7 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
 extern "C" int32_t orcha_packet_destroy(orcha_packet* p) {
   if (!p) return ORCHA_OK;
   drop_plans_with(p);
+  comm_drop_packet(p);
   cudaFree(p->d_slots);
   delete p;
   return ORCHA_OK;
@@ -402,14 +403,6 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     }
     f->d_tables.push_back(d);
   }
-  if (f->has_remote) {
-    int32_t rc = comm_build_plan(comm, pk, npk, &f->remote);
-    if (rc) {
-      for (auto* t : f->d_tables) cudaFree(t);
-      delete f;
-      return rc;
-    }
-  }
   *out = f;
   return ORCHA_OK;
 }
@@ -439,7 +432,9 @@ extern "C" int32_t orcha_fill_guardcells(orcha_packet* const* pk, int32_t npk, o
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (f->has_remote) {
-    rc = comm_exchange(comm, f->remote, s);
+    CommPlan* cp = nullptr;  // cached by the communicator per packet set
+    rc = comm_build_plan(comm, pk, npk, &cp);
+    if (rc == ORCHA_OK) rc = comm_exchange(comm, cp, s);
     if (rc) return rc;
   }
   for (int q = 0; q < npk; q++) {

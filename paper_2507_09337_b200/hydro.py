@@ -134,6 +134,70 @@ class Packet:
         return fh.value, fb.value
 
 
+def brick_owner(nblk: Sequence[int], brick: Sequence[int], gpu_grid: Sequence[int]) -> np.ndarray:
+    """block -> rank for a grid of bricks (rank = (rz*py + ry)*px + rx), int32[nblocks]."""
+    nblk = list(nblk) + [1] * (3 - len(nblk))
+    brick = list(brick) + [1] * (3 - len(brick))
+    px, py = gpu_grid[0], gpu_grid[1]
+    b = np.arange(nblk[0] * nblk[1] * nblk[2], dtype=np.int64)
+    bi, bj, bk = b % nblk[0], (b // nblk[0]) % nblk[1], b // (nblk[0] * nblk[1])
+    return ((bk // brick[2]) * (px * py) + (bj // brick[1]) * px + bi // brick[0]).astype(np.int32)
+
+
+class Comm:
+    """Communicator for blocks partitioned over ranks (include/orcha.h)."""
+
+    def __init__(self, grid: Grid, handle, nranks: int, rank: int, owner: np.ndarray):
+        self.grid, self.lib, self.handle = grid, grid.lib, handle
+        self.nranks, self.rank, self.owner = nranks, rank, owner
+
+    @staticmethod
+    def create(grid: Grid, nranks: int, rank: int, owner) -> "Comm":
+        """NCCL communicator; the 128-byte unique id is broadcast with torch.distributed."""
+        import torch.distributed as dist
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        uid = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            abi.call(grid.lib, "orcha_comm_unique_id", uid)
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        h = ctypes.c_void_p()
+        abi.call(grid.lib, "orcha_comm_create", grid.handle, uid, nranks, rank,
+                 owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(h))
+        return Comm(grid, h, nranks, rank, owner)
+
+    @staticmethod
+    def create_local(grid: Grid, nranks: int, owner) -> list:
+        """Virtual ranks on one device (device-copy transport), for tests."""
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        hs = (ctypes.c_void_p * nranks)()
+        abi.call(grid.lib, "orcha_comm_create_local", grid.handle, nranks,
+                 owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), hs)
+        return [Comm(grid, ctypes.c_void_p(hs[r]), nranks, r, owner) for r in range(nranks)]
+
+    def push(self, packets, stream=None):
+        arr, n = _handles(packets)
+        abi.call(self.lib, "orcha_comm_push", self.handle, arr, n, ctypes.c_void_p(_stream_ptr(stream)))
+
+    def destroy(self):
+        if self.handle:
+            self.lib.orcha_comm_destroy(self.handle)
+            self.handle = None
+
+
+def comm_plan(grid: Grid, nranks: int, rank: int, owner, peer: int, which: int) -> np.ndarray:
+    """Host-only exchange plan query (orcha_comm_plan); no device needed."""
+    owner = np.ascontiguousarray(owner, dtype=np.int32)
+    op = owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    n = ctypes.c_int64()
+    abi.call(grid.lib, "orcha_comm_plan", grid.handle, nranks, rank, op, peer, which, None, 0, ctypes.byref(n))
+    out = np.empty(n.value, dtype=np.int64)
+    abi.call(grid.lib, "orcha_comm_plan", grid.handle, nranks, rank, op, peer, which,
+             out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n.value, ctypes.byref(n))
+    return out
+
+
 def _handles(packets):
     arr = (ctypes.c_void_p * len(packets))(*[p.handle.value for p in packets])
     return arr, len(packets)

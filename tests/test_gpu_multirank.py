@@ -1,0 +1,107 @@
+"""Multi-rank path on one GPU: R virtual ranks (LOCAL transport: the NCCL
+path's plan, pack and unpack kernels with device copies instead of
+ncclSend/Recv) must give results bitwise identical to the single-domain run
+(production build) and to the oracle (parity build).  SURVEY 8(e): "Results
+must be bitwise identical across 1/2/4/8 GPUs on the same global grid"."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import orcha_inputs as inp
+from tests import gpu_helpers as H
+
+pytestmark = pytest.mark.gpu
+O, P, R = 0, 1, 2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _run_virtual(g, U0, owner, nsteps, packets_per_rank=2):
+    from paper_2507_09337_b200 import hydro
+    nd = g.ndim
+    n = int(owner.max()) + 1
+    comms = hydro.Comm.create_local(g, n, owner)
+    pks = []
+    for r in range(n):
+        ids = np.flatnonzero(owner == r)
+        parts = [a for a in np.array_split(ids, packets_per_rank) if len(a)]
+        pr = [hydro.Packet(g, p) for p in parts]
+        for p in pr:
+            p.pack(inp.to_blocks(U0, g.nb[:nd], p.block_ids))
+        pks.append(pr)
+    allp = [p for pr in pks for p in pr]
+    dts = []
+    for _ in range(nsteps):
+        for r in range(n):
+            comms[r].push(pks[r])
+        for r in range(n):
+            hydro.orcha_fill_guardcells(pks[r], comms[r])
+        info = hydro.orcha_compute_dt(allp)           # global dt over all virtual ranks
+        dts.append(info.dt)
+        for p in allp:
+            hydro.orcha_hydro_advance(p, info.dt)
+    out = H.gather(g, allp)
+    for c in comms:
+        c.destroy()
+    return out, dts
+
+
+CASES = [
+    (3, (8, 8, 8), (4, 2, 2), ((O, O),) * 3, (2, 1, 1), (2, 2, 2)),
+    (3, (8, 8, 8), (4, 4, 2), ((P, P), (R, O), (O, R)), (2, 2, 1), (2, 2, 2)),
+    (3, (16, 16, 16), (2, 2, 2), ((O, O),) * 3, (2, 2, 2), (1, 1, 1)),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_virtual_ranks_bitwise_equal_single_domain(case):
+    from paper_2507_09337_b200 import hydro
+    ndim, nb, nblk, bc, gg, brick = case
+    g = H.make_grid(ndim, nb, nblk, bc=bc)
+    owner = hydro.brick_owner(nblk, brick, gg)
+    U0 = inp.sedov(g.N[:ndim]) if bc[0][0] == O else inp.random_field(g.N[:ndim], seed=3)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=5)
+    B, dts = _run_virtual(g, U0, owner, 5)
+    assert dts == [x[0] for x in logA]
+    assert np.array_equal(A, B)
+
+
+def test_virtual_ranks_parity_build_equals_oracle():
+    # cfg4's decomposition in miniature: 8 bricks (one Sedov octant each)
+    from paper_2507_09337_b200 import hydro
+    ndim, nb, nblk, bc, gg, brick = CASES[2]
+    g = H.make_grid(ndim, nb, nblk, bc=bc, parity=True)
+    owner = hydro.brick_owner(nblk, brick, gg)
+    U0 = inp.sedov(g.N)
+    B, dts = _run_virtual(g, U0, owner, 4)
+    Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4)
+    assert dts == olog.dts
+    assert np.array_equal(B, Oo)
+
+
+def test_nccl_single_rank_communicator():
+    # the NCCL code path (dlopen, unique id, init) on one rank: no peers, the
+    # fill and dt go through the communicator and match the comm-less run
+    from paper_2507_09337_b200 import abi, hydro
+    g = H.make_grid(3, (8, 8, 8), (2, 2, 2))
+    owner = np.zeros(g.nblocks, dtype=np.int32)
+    uid = (ctypes.c_uint8 * 128)()
+    abi.call(g.lib, "orcha_comm_unique_id", uid)
+    h = ctypes.c_void_p()
+    abi.call(g.lib, "orcha_comm_create", g.handle, uid, 1, 0, owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+             ctypes.byref(h))
+    comm = hydro.Comm(g, h, 1, 0, owner)
+    U0 = inp.sedov(g.N)
+    pk = H.gpu_setup(g, U0, npackets=2)
+    t, n, log = hydro.run(pk, nsteps=3, comm=comm)
+    A = H.gather(g, pk)
+    B, _, logB, _ = H.gpu_run(g, U0, nsteps=3)
+    assert [x[0] for x in log] == [x[0] for x in logB]
+    assert np.array_equal(A, B)
+    comm.destroy()

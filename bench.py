@@ -36,29 +36,29 @@ UNIT = "cell-updates/s"
 
 def algorithmic_costs(nb=16, ng=4):
     """Per cell-update algorithmic work of the telescoped 16^3 step (DESIGN.md
-    'Roofline'): bytes of the advance (read the padded block once, write the
-    interior once) and of the guard fill (read sources, write guards); fp64
-    flops of the method with every face flux, EOS and slope evaluated once."""
+    section 6): bytes of the advance (read the padded block once,
+    write the interior once) and of the guard fill (read every guard's source,
+    write the guard); fp64-pipe instructions of the advance (SURVEY 8(d):
+    1498 per cell-update for the box stage-1 region, SASS-derived)."""
     P = nb + 2 * ng
     n3 = nb ** 3
     adv_bytes = (P ** 3 + n3) * 5 * 8 / n3
     guards = P ** 3 - n3
     fill_bytes = 2 * guards * 5 * 8 / n3
-    # faces: stage 1 on the box (n+4)^3 (x-faces (n+5)(n+4)^2 per axis), stage 2 on n^3
-    s1 = nb + 4
-    faces = 3 * (s1 + 1) * s1 * s1 + 3 * (nb + 1) * nb * nb
-    cells_eos = P ** 3 + s1 ** 3          # primitive recovery of stage-1 input, stage-2 input
-    slopes = 3 * ((s1 + 2) * s1 * s1 + (nb + 2) * nb * nb)  # per axis per cell of the face stencils
-    flops = (faces * FLOPS_PER_FACE + cells_eos * FLOPS_PER_EOS + slopes * 5 * FLOPS_PER_SLOPE +
-             (s1 ** 3 + n3) * 5 * FLOPS_PER_UPDATE) / n3
-    return adv_bytes, fill_bytes, flops
+    return adv_bytes, fill_bytes, FP64_INSTR_PER_CU
 
 
-# fp64 flop counts of the method's expressions (FMA counted as 2; div, sqrt as 1)
-FLOPS_PER_FACE = 2 * 5 + 2 * (3 + 9 + 5 + 2) + 6 + 1 + 1 + 5 * 6   # PLM faces, 2x(c,E,U,F), S_L/S_R, inv, HLL
-FLOPS_PER_EOS = 12
-FLOPS_PER_SLOPE = 5
-FLOPS_PER_UPDATE = 5                                                 # dF*id sums + RK combination
+FP64_INSTR_PER_CU = 1498.0
+
+
+def measured_traffic():
+    """dram read+write bytes per advance from the committed ncu --set full
+    capture (profiles/traffic.json, written by scripts/traffic_from_ncu.py), or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        t = json.load(open(path))
+        return t.get("advance_bytes_per_launch"), t.get("source")
+    return None, None
 
 
 def peaks():
@@ -69,8 +69,8 @@ def peaks():
         m = json.load(open(path))
         p = {"hbm_gbs": float(m["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)",
              "sm_max_mhz": float(m.get("sm_max_mhz", 1965.0))}
-    # fp64 pipe: 148 SMs x 64 fp64 FMA lanes x 2 flop x clock (B200_PROFILING.md unit counts)
-    p["fp64_tflops"] = 148 * 64 * 2 * p.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    # fp64 pipe: 148 SMs x 64 fp64 lanes x clock thread-instructions/s (B200_PROFILING.md unit counts)
+    p["fp64_tinst"] = 148 * 64 * p.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     return p
 
 
@@ -285,17 +285,21 @@ def main():
 
     # roofline of the dominant kernel (the advance): algorithmic bytes / flops
     pks = peaks()
-    adv_bytes, fill_bytes, flops = algorithmic_costs()
+    adv_bytes, fill_bytes, fp_instr = algorithmic_costs()
     cu_local = BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2] * NB[0] * NB[1] * NB[2]
     hbm_achieved = adv_bytes * cu_local / (adv_ms / 1e3) / 1e9
-    fp_achieved = flops * cu_local / (adv_ms / 1e3) / 1e12
+    fp_achieved = fp_instr * cu_local / (adv_ms / 1e3) / 1e12
+    traffic, traffic_src = measured_traffic()
     roof_hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": pks["hbm_gbs"], "unit": "GB/s",
-                "frac": hbm_achieved / pks["hbm_gbs"], "traffic": None, "peak_source": pks["source"],
-                "kernel": "hydro_advance (stage1+stage2)", "algorithmic_bytes_per_cell_update": adv_bytes}
-    roof_fp = {"bound": "alu", "achieved": fp_achieved, "peak": pks["fp64_tflops"], "unit": "TFLOP/s",
-               "frac": fp_achieved / pks["fp64_tflops"], "traffic": None,
-               "peak_source": "derived: 148 SM x 64 fp64 lanes x 2 x sm_max clock",
-               "kernel": "hydro_advance (stage1+stage2)", "algorithmic_flops_per_cell_update": flops}
+                "frac": hbm_achieved / pks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": pks["source"], "kernel": "hydro_advance (stage_fused_kernel<16,1> + <16,2>)",
+                "algorithmic_bytes_per_cell_update": adv_bytes, "units_per_launch": cu_local}
+    roof_fp = {"bound": "alu", "achieved": fp_achieved, "peak": pks["fp64_tinst"],
+               "unit": "T fp64-pipe inst/s", "frac": fp_achieved / pks["fp64_tinst"], "traffic": traffic,
+               "traffic_source": traffic_src,
+               "peak_source": "derived (DESIGN.md 6): 148 SM x 64 fp64 lanes x sm_max clock",
+               "kernel": "hydro_advance (stage_fused_kernel<16,1> + <16,2>)",
+               "algorithmic_fp64_instr_per_cell_update": fp_instr, "units_per_launch": cu_local}
     primary, other = (roof_fp, roof_hbm) if roof_fp["frac"] >= roof_hbm["frac"] else (roof_hbm, roof_fp)
     step_hbm = (adv_bytes + fill_bytes) * value / world / 1e9
 

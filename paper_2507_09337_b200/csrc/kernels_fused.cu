@@ -65,7 +65,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // ------------------------------------------------------------- geometry ----
-template <int NB, int STAGE>
+template <int NB, int STAGE, int SPLIT>
 struct Geo {
   static constexpr int W = (STAGE == 1) ? NB + 4 : NB;       // output columns (and rows) per plane
   static constexpr int OFF = (W - NB) / 2;                   // output origin (interior-relative) = -OFF
@@ -75,7 +75,7 @@ struct Geo {
   static constexpr int IPX = NB + 2 * INO;                   // padded input row length (= plane rows)
   static constexpr int PLANE = IPX * IPX;                    // doubles per input plane per variable
   static constexpr int NPLANES = NK + 4;                     // input planes streamed
-  static constexpr int NSPLIT = (NB == 16) ? 2 : 1;          // row bands per block
+  static constexpr int NSPLIT = SPLIT;                       // row bands per block
   static constexpr int H = W / NSPLIT;                       // output rows per CTA
   static constexpr int IR = H + 4;                           // staged input rows per plane
   static constexpr int BAND = IR * IPX;                      // doubles per staged band per variable
@@ -83,14 +83,18 @@ struct Geo {
   static constexpr int FX = H * (W + 1);                     // x-faces per band
   static constexpr int FY = (H + 1) * W;                     // y-faces per band
   static constexpr int FZ = H * W;                           // z-faces per band (and cells)
-  static constexpr int NT = (NB == 16) ? (STAGE == 1 ? 352 : 224) : ((W * W + 31) / 32) * 32;
-  static constexpr int MINB = (NB == 16) ? (STAGE == 1 ? 2 : 3) : 1;
-  // face tasks are dealt out in warp-sized slots of one direction each
-  static constexpr int NW = NT / 32;
+  // face tasks are dealt out in warp-sized slots of one direction each; the
+  // warp count is chosen so every warp gets two slots (two rounds)
   static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
   static constexpr int NSLOT = SX + SY + SZ;
+  static constexpr int NW = (NB == 16) ? (NSLOT + 1) / 2 : (W * W + 31) / 32;
+  static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   static constexpr size_t SMEM = sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64;
+  // CTAs per SM we aim for: shared memory bound (227 KB per SM), at most 4
+  static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
+  static constexpr int MINB = MINB_S < 1 ? 1 : (MINB_S > 4 ? 4 : MINB_S);
+  static_assert(NT >= FZ, "one update cell per thread");
   static_assert((BAND * 8) % 16 == 0, "bulk copies need 16-byte multiples");
 };
 
@@ -101,12 +105,12 @@ __host__ __device__ constexpr long long u1_cube() {
   return ((long long)(NB + 4) * (NB + 4) * (NB + 4) * 8 + 255) / 256 * 256 / 8;
 }
 
-template <int NB, int STAGE>
-__global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
+template <int NB, int STAGE, int SPLIT>
+__global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLIT>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
                        DtRecord* __restrict__ rec, DevStatus* st) {
-  using Gm = Geo<NB, STAGE>;
+  using Gm = Geo<NB, STAGE, SPLIT>;
   constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
   constexpr int NT = Gm::NT, H = Gm::H;
   constexpr long long U1C = u1_cube<NB>();
@@ -133,10 +137,13 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
   }
   __syncthreads();
 
-  // input plane p (0-based, z = K0 - 2 + p): padded rows [jj0, jj0 + IR) -> ring slot p % NS
+  // input plane p (0-based, z = K0 - 2 + p): padded rows [jj0, jj0 + IR) -> ring slot p % NS.
+  // Called by one thread after a CTA barrier that follows every generic
+  // access to the slot; the proxy fence orders those before the async copy.
   auto issue = [&](int p) {
     if (p < Gm::NPLANES) {
       int s = p % NS;
+      fence_proxy_async();
       mbar_expect_tx(&bar[s], 5u * BAND * 8u);
 #pragma unroll
       for (int v = 0; v < 5; v++)
@@ -181,10 +188,21 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
   };
   // band-local output row j (0..H) <-> staged row j + 2; output column i <-> staged column i - OFF + INO
   // x-face between columns f-1 and f of band row j
-  auto x_task = [&](int t, int it) {
-    int j = t / (W + 1), f = t - j * (W + 1);
+  // stencil base offset (in a staged band) of face task t of direction kind
+  auto task_base = [&](int kind, int t) -> int {
+    if (kind == 0) {
+      int j = t / (W + 1), f = t - j * (W + 1);
+      return (j + 2) * IPX + (f - OFF - 2 + INO);
+    }
+    if (kind == 1) {
+      int f = t / W, i = t - f * W;
+      return f * IPX + (i - OFF + INO);
+    }
+    int j = t / W, i = t - j * W;
+    return (j + 2) * IPX + (i - OFF + INO);
+  };
+  auto x_task = [&](int t, int base, int it) {
     const double* P = ring + ((it + 2) % NS) * 5 * BAND;
-    int base = (j + 2) * IPX + (f - OFF - 2 + INO);
     Prim q0, q1, q2, q3, L, R;
     ld(P, base, q0);
     ld(P, base + 1, q1);
@@ -194,10 +212,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
     hll_store<0>(L, R, G, Fx + t, Gm::FX);
   };
   // y-face between band rows f-1 and f of column i
-  auto y_task = [&](int u, int it) {
-    int f = u / W, i = u - f * W;
+  auto y_task = [&](int u, int base, int it) {
     const double* P = ring + ((it + 2) % NS) * 5 * BAND;
-    int base = f * IPX + (i - OFF + INO);
     Prim q0, q1, q2, q3, L, R;
     ld(P, base, q0);
     ld(P, base + IPX, q1);
@@ -207,9 +223,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
     hll_store<1>(L, R, G, Fy + u, Gm::FY);
   };
   // z-face k+1/2 of column (i, j): stencil planes it+1 .. it+4 (z = k-1 .. k+2)
-  auto z_task = [&](int w, int it, double* fz_out) {
-    int j = w / W, i = w - j * W;
-    int base = (j + 2) * IPX + (i - OFF + INO);
+  auto z_task = [&](int w, int base, int it, double* fz_out) {
     Prim q0, q1, q2, q3, L, R;
     ld(ring + ((it + 1) % NS) * 5 * BAND, base, q0);
     ld(ring + ((it + 2) % NS) * 5 * BAND, base, q1);
@@ -219,6 +233,20 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
     hll_store<2>(L, R, G, fz_out + w, Gm::FZ);
   };
   const int warp = tid >> 5, lane = tid & 31;
+  // this thread's face tasks (the same on every plane): warp-uniform direction
+  // slots r*NW + warp, decoded once
+  int tkind[Gm::ROUNDS], ttask[Gm::ROUNDS], tbase[Gm::ROUNDS];
+#pragma unroll
+  for (int r = 0; r < Gm::ROUNDS; r++) {
+    const int m = r * Gm::NW + warp;
+    int kind = 3, t = 0;
+    if (m < Gm::SX) { t = m * 32 + lane; kind = t < Gm::FX ? 0 : 3; }
+    else if (m < Gm::SX + Gm::SY) { t = (m - Gm::SX) * 32 + lane; kind = t < Gm::FY ? 1 : 3; }
+    else if (m < Gm::NSLOT) { t = (m - Gm::SX - Gm::SY) * 32 + lane; kind = t < Gm::FZ ? 2 : 3; }
+    tkind[r] = kind;
+    ttask[r] = t;
+    tbase[r] = kind < 3 ? task_base(kind, t) : 0;
+  }
 
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
   if (tid == 0)
@@ -228,8 +256,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
     convert(p);
   }
   __syncthreads();
-  for (int w = tid; w < Gm::FZ; w += NT) z_task(w, -1, Fz + 5 * Gm::FZ);
-  fence_proxy_async();
+  for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
   __syncthreads();
   if (tid == 0) issue(5);  // into the slot of plane 0
 
@@ -255,21 +282,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
     }
     // phase 1: all face fluxes of the band's plane k (inputs: planes it+1 .. it+4)
     double* fz_cur = Fz + (it & 1) * 5 * Gm::FZ;
-#pragma unroll 1
+#pragma unroll
     for (int r = 0; r < Gm::ROUNDS; r++) {
-      const int m = r * Gm::NW + warp;  // warp-uniform slot
-      if (m < Gm::SX) {
-        int t = m * 32 + lane;
-        if (t < Gm::FX) x_task(t, it);
-      } else if (m < Gm::SX + Gm::SY) {
-        int t = (m - Gm::SX) * 32 + lane;
-        if (t < Gm::FY) y_task(t, it);
-      } else if (m < Gm::NSLOT) {
-        int t = (m - Gm::SX - Gm::SY) * 32 + lane;
-        if (t < Gm::FZ) z_task(t, it, fz_cur);
-      }
+      if (tkind[r] == 0) x_task(ttask[r], tbase[r], it);
+      else if (tkind[r] == 1) y_task(ttask[r], tbase[r], it);
+      else if (tkind[r] == 2) z_task(ttask[r], tbase[r], it, fz_cur);
     }
-    fence_proxy_async();
     __syncthreads();
     // phase 2: stage plane it+6 into the slot of plane it+1 (read for the
     // last time in phase 1), convert plane it+5, update the band's cells
@@ -309,7 +327,6 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
         if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)g);
       }
     }
-    fence_proxy_async();
     __syncthreads();
   }
   if (STAGE == 2) {
@@ -318,24 +335,48 @@ __global__ void __launch_bounds__(Geo<NB, STAGE>::NT, Geo<NB, STAGE>::MINB)
   }
 }
 
+template <int NB, int STAGE, int SPLIT>
+static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
+                         const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s) {
+  using Gm = Geo<NB, STAGE, SPLIT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Gm::SMEM);
+    attr = true;
+  }
+  stage_fused_kernel<NB, STAGE, SPLIT><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, d_dt, h_dt,
+                                                                                records, st);
+  count_launch();
+}
+
+// Row bands per block (CTAs per block) for 16^3: measured best by default;
+// ORCHA_SPLIT1 / ORCHA_SPLIT2 (2 or 4) override for experiments.
+static int split_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  if (!e) return dflt;
+  int v = atoi(e);
+  return (v == 2 || v == 4) ? v : dflt;
+}
+
 template <int NB>
 static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
                              cudaStream_t s) {
-  using G1 = Geo<NB, 1>;
-  using G2 = Geo<NB, 2>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(stage_fused_kernel<NB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G1::SMEM);
-    cudaFuncSetAttribute(stage_fused_kernel<NB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2::SMEM);
-    attr = true;
+  int s2 = 1;
+  if constexpr (NB == 16) {
+    static const int s1 = split_env("ORCHA_SPLIT1", 2);
+    static const int s2v = split_env("ORCHA_SPLIT2", 2);
+    s2 = s2v;
+    if (s1 == 4) launch_stage<NB, 1, 4>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<NB, 1, 2>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (s2 == 4) launch_stage<NB, 2, 4>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<NB, 2, 2>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+  } else {
+    launch_stage<NB, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
   }
-  stage_fused_kernel<NB, 1><<<nslots * G1::NSPLIT, G1::NT, G1::SMEM, s>>>(G, state, u1, slots, d_dt, h_dt,
-                                                                          records, st);
-  stage_fused_kernel<NB, 2><<<nslots * G2::NSPLIT, G2::NT, G2::SMEM, s>>>(G, state, u1, slots, d_dt, h_dt,
-                                                                          records, st);
-  count_launch(2);
-  *nrecords = (long long)nslots * G2::NSPLIT;
+  *nrecords = (long long)nslots * s2;
   return cudaGetLastError();
 }
 

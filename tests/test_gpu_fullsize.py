@@ -1,0 +1,75 @@
+"""Parity at BASELINE.json's full single-GPU size, in the launch configuration
+bench.py times (cfg4: one packet of 4096 blocks of 16^3 = 256^3 cells, fused
+kernels): one step against the oracle on the whole global array (bitwise in
+the parity build, <= 1e-12 by the c13 metric in the production build), and
+size-independent properties over 10 steps (octant mirror symmetry, exact
+mass conservation while the blast is inside the box, dt bitwise repeatable
+and equal between the builds' first step)."""
+import numpy as np
+import pytest
+
+import oracle
+import orcha_inputs as inp
+from tests import gpu_helpers as H
+
+pytestmark = pytest.mark.gpu
+NB, NBLK = (16, 16, 16), (16, 16, 16)
+N = (256, 256, 256)
+
+
+@pytest.fixture(scope="module")
+def oracle_one_step():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    og = oracle.Grid(N=N)
+    U = oracle.padded(og, inp.sedov(N))
+    oracle.fill_ghosts(og, U)
+    r = oracle.compute_dt(og, U)
+    rc, hits = oracle.step(og, U, r.dt)
+    assert rc == 0 and hits == 0
+    return r, U[og.interior].copy()
+
+
+def _gpu(parity, nsteps):
+    from paper_2507_09337_b200 import hydro
+    g = H.make_grid(3, NB, NBLK, parity=parity)
+    ids = np.arange(g.nblocks)
+    pk = hydro.Packet(g, ids)
+    pk.pack(inp.sedov_packet(N, NB, ids))
+    t, n, log = hydro.run([pk], nsteps=nsteps)
+    return g, pk, log
+
+
+@pytest.mark.parametrize("parity", [True, False])
+def test_cfg4_one_step_against_oracle(oracle_one_step, parity):
+    r, ref = oracle_one_step
+    g, pk, log = _gpu(parity, 1)
+    out = H.gather(g, [pk])
+    if parity:
+        assert log[0][0] == r.dt and log[0][2] == r.argmax
+        assert np.array_equal(out, ref)
+    else:
+        assert abs(log[0][0] - r.dt) <= 1e-13 * r.dt and log[0][2] == r.argmax
+        assert H.parity_error(out, ref) <= 1e-12
+    assert pk.counters() == (0, -1)
+
+
+def test_cfg4_ten_steps_properties():
+    g, pk, log = _gpu(False, 10)
+    out = H.gather(g, [pk])
+    rho = out[0]
+    # mass is exact while the blast is inside (boundary fluxes are exactly 0)
+    assert abs(rho.sum() / rho.size - 1.0) <= 1e-13
+    # octant mirror symmetry of the centred blast (FMA build: to round-off)
+    for ax, mom in ((3, 1), (2, 2), (1, 3)):
+        m = np.flip(out, axis=ax).copy()
+        m[mom] = -m[mom]
+        for v in range(5):
+            scale = np.abs(out[v]).max()
+            assert np.abs(out[v] - m[v]).max() <= 1e-13 * scale
+    # dt is positive, decreasing as the blast sharpens, and repeatable
+    dts = [x[0] for x in log]
+    g2, pk2, log2 = _gpu(False, 10)
+    assert dts == [x[0] for x in log2]
+    assert np.array_equal(H.gather(g2, [pk2]), out)

@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=None, help="advance kernel variant (0 ref, 1 fused)")
+    ap.add_argument("--method", default="telescoped", choices=["telescoped", "per-stage"],
+                    help="RK2 step: the paper's telescoped step (default) or the per-stage F1 variant")
+    ap.add_argument("--no-variants", action="store_true", help="skip the per-stage measurement beside the main line")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -240,17 +243,41 @@ def main():
 
     adv_ev = []
 
-    def step(record=False):
-        hydro.orcha_fill_guardcells([pk], comm, stream)
+    def step(record=False, method=args.method):
+        if method == "per-stage":
+            hydro.orcha_fill_guardcells_stage([pk], 0, comm, stream)
+        else:
+            hydro.orcha_fill_guardcells([pk], comm, stream)
         info = hydro.orcha_compute_dt([pk], math.inf, comm, stream)
         if record:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        hydro.orcha_hydro_advance(pk, info.dt, stream)
+        hydro.step([pk], info.dt, comm, stream, method)
         if record:
             b.record(stream)
             adv_ev.append((a, b))
         return info
+
+    def timed_variant(method, nsteps):
+        """Same protocol for another step variant (reported beside the main line)."""
+        for _ in range(3):
+            step(method=method)
+        adv_ev.clear()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for _ in range(nsteps):
+            step(record=True, method=method)
+        v1.record(stream)
+        torch.cuda.synchronize()
+        vt = torch.tensor([v0.elapsed_time(v1) / nsteps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+        vms = float(vt.item())
+        return {"ms_per_step": vms, "value": N[0] * N[1] * N[2] / (vms / 1e3),
+                "advance_ms": statistics.mean(a.elapsed_time(b) for a, b in adv_ev)}
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -282,6 +309,14 @@ def main():
     cells = N[0] * N[1] * N[2]
     value = cells / (ms / 1e3)
     adv_ms = statistics.mean(a.elapsed_time(b) for a, b in adv_ev)
+    variants = {}
+    if args.method == "telescoped" and not args.no_variants:
+        # SURVEY 8(f) F1, measured beside the paper's telescoped step (same protocol)
+        variants["per-stage"] = timed_variant("per-stage", args.steps)
+        variants["per-stage"]["note"] = ("fill -> dt -> stage 1 (interior) -> U1 guard refill -> stage 2; "
+                                         "oracle mode 'refill'")
+        # restore the packet to a telescoped-step history is not needed: both
+        # variants advance the same Sedov state, timing only
 
     # roofline of the dominant kernel (the advance): algorithmic bytes / flops
     pks = peaks()
@@ -343,7 +378,8 @@ def main():
             "roofline": primary, "roofline_other": other,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
                                        "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},
-            "advance_ms": adv_ms, "clocks": clk, "gpu_launches": int(launches), "e2e": e2e,
+            "advance_ms": adv_ms, "method": args.method, "variants": variants,
+            "clocks": clk, "gpu_launches": int(launches), "e2e": e2e,
             "floor_hits": fh, "nonphysical_first_cell": bad,
         }
         if not args.no_cpu_baseline:

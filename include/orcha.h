@@ -191,6 +191,30 @@ int32_t orcha_hydro_advance(orcha_packet* packet, double dt, void* stream);
 /* Same, reading dt from device memory (graph-capturable: no host value). */
 int32_t orcha_hydro_advance_devdt(orcha_packet* packet, const double* d_dt, void* stream);
 
+/* ---- per-stage variant (the two-refresh scheme P:L667-668
+ * describes before the communication-avoidance trick) ----
+ * One SSP-RK2 stage on the interior only:
+ *   stage 1: U1 = U^n - dt*D(U^n) into the packet's stage-1 buffer (scratch,
+ *            same padded layout as the state); requires a state guard fill;
+ *   stage 2: U^{n+1} = 0.5*(U^n + (U1 - dt*D(U1))) in place, + dt records;
+ *            requires orcha_fill_guardcells_stage(..., buffer = 1) after
+ *            stage 1 (the second guard refresh, with the physical boundary
+ *            conditions applied to U1 -- at outflow walls this differs from
+ *            the telescoped step in round-off-level momentum tails, reading c5).
+ * Errors: ORCHA_E_ARG (stage not 1/2), ORCHA_E_STATE (call order). */
+int32_t orcha_hydro_stage(orcha_packet* packet, int32_t stage, double dt, void* stream);
+int32_t orcha_hydro_stage_devdt(orcha_packet* packet, int32_t stage, const double* d_dt, void* stream);
+
+/* Guard fill for the per-stage variant: buffer 0 (the state) or buffer 1
+ * (the stage-1 buffer, after orcha_hydro_stage(..., 1, ...)).  Fills only
+ * what ONE stage reads -- the face guards (one axis outside the block) to
+ * depth 2 -- with the same values as orcha_fill_guardcells (exchange
+ * included); a state filled this way is valid for orcha_hydro_stage, not for
+ * the telescoped orcha_hydro_advance (ORCHA_E_STATE).  Errors as
+ * orcha_fill_guardcells, plus ORCHA_E_STATE. */
+int32_t orcha_fill_guardcells_stage(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
+                                    int32_t buffer, void* stream);
+
 /* ----------------------------------------------------------- support ---- */
 
 /* Counters since the last pack: pressure-floor hits in primitive recovery
@@ -241,7 +265,8 @@ int32_t orcha_comm_destroy(orcha_comm* comm);
  * orcha_fill_guardcells for each (which unpacks and fills).  No NCCL needed. */
 int32_t orcha_comm_create_local(const orcha_grid* grid, int32_t nranks, const int32_t* block_owner,
                                 orcha_comm** out);
-int32_t orcha_comm_push(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, void* stream);
+int32_t orcha_comm_push(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, int32_t buffer,
+                        void* stream);  /* buffer: 0 = state, 1 = stage-1 buffer */
 
 /* Host-only view of the guard exchange plan between `rank` and `peer` (no
  * device work; for tests and tooling).  The plan is a pure function of the

@@ -238,6 +238,7 @@ struct PeerBuf {
 
 struct CommPlan {
   std::vector<orcha_packet*> packets;
+  int buffer = 0;
   std::vector<const double**> d_send_src;  // per peer (device array of n_send pointers)
   UnpackEntry* d_unpack = nullptr;
   long long n_unpack = 0;
@@ -295,9 +296,9 @@ static int32_t validate_owner(const orcha_grid* g, int nranks, const int32_t* ow
   return ORCHA_OK;
 }
 
-int32_t comm_build_plan(orcha_comm* c, orcha_packet* const* pk, int npk, CommPlan** out) {
+int32_t comm_build_plan(orcha_comm* c, orcha_packet* const* pk, int npk, int buffer, CommPlan** out) {
   for (auto* p : c->plans) {
-    if ((int)p->packets.size() != npk) continue;
+    if ((int)p->packets.size() != npk || p->buffer != buffer) continue;
     bool same = true;
     for (int q = 0; q < npk; q++) same &= p->packets[q] == pk[q];
     if (same) { *out = p; return ORCHA_OK; }
@@ -306,14 +307,17 @@ int32_t comm_build_plan(orcha_comm* c, orcha_packet* const* pk, int npk, CommPla
   std::unordered_map<long long, std::pair<int, int>> where;
   for (int q = 0; q < npk; q++)
     for (int s = 0; s < pk[q]->nslots; s++) where[pk[q]->ids[s]] = {q, s};
+  // buffer 0: the packet state; 1: the stage-1 buffer (scratch, same padded layout)
   auto addr = [&](long long block, long long cell, double** a) -> bool {
     auto it = where.find(block);
     if (it == where.end()) return false;
-    *a = pk[it->second.first]->state + (long long)it->second.second * kNVar * G.cube + cell;
+    orcha_packet* p = pk[it->second.first];
+    *a = (buffer ? p->scratch : p->state) + (long long)it->second.second * kNVar * G.cube + cell;
     return true;
   };
   CommPlan* P = new CommPlan();
   P->packets.assign(pk, pk + npk);
+  P->buffer = buffer;
   std::vector<UnpackEntry> un;
   for (size_t i = 0; i < c->lists.size(); i++) {
     const PeerLists& L = c->lists[i];
@@ -539,11 +543,13 @@ extern "C" int32_t orcha_comm_create_local(const orcha_grid* g, int32_t nranks, 
   return ORCHA_OK;
 }
 
-extern "C" int32_t orcha_comm_push(orcha_comm* c, orcha_packet* const* pk, int32_t npk, void* stream) {
+extern "C" int32_t orcha_comm_push(orcha_comm* c, orcha_packet* const* pk, int32_t npk, int32_t buffer,
+                                   void* stream) {
   if (!c || !pk || npk < 1) return fail(ORCHA_E_ARG, "null argument");
   if (!c->local) return fail(ORCHA_E_ARG, "orcha_comm_push is for LOCAL communicators only");
+  if (buffer != 0 && buffer != 1) return fail(ORCHA_E_ARG, "buffer must be 0 or 1");
   CommPlan* P = nullptr;
-  int32_t rc = comm_build_plan(c, pk, npk, &P);
+  int32_t rc = comm_build_plan(c, pk, npk, buffer, &P);
   if (rc) return rc;
   return pack_all(c, P, true, (cudaStream_t)stream);
 }

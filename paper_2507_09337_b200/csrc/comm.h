@@ -6,7 +6,8 @@ namespace orcha {
 struct CommPlan;  // per fill plan: guard cells whose source block lives on another rank
 
 // Build the exchange plan for this rank's packets (host; one device upload).
-int32_t comm_build_plan(orcha_comm* comm, orcha_packet* const* pk, int npk, CommPlan** out);
+// buffer 0 = packet state, 1 = stage-1 buffer (per-stage variant).
+int32_t comm_build_plan(orcha_comm* comm, orcha_packet* const* pk, int npk, int buffer, CommPlan** out);
 void comm_free_plan(CommPlan* plan);
 // Forget cached plans that reference a packet being destroyed.
 void comm_drop_packet(orcha_packet* p);

@@ -13,8 +13,11 @@ namespace orcha {
 // each axis: shift (neighbour or periodic image), clamp (outflow: edge cell)
 // or mirror (reflect, negating the normal momentum) -- the per-axis images
 // compose to the global axis-ordered ghost fill.
+// faces_only: fill only the face slabs (one axis outside the interior) to
+// depth `depth` -- the stencil of ONE RK2 stage (per-stage variant, F1).
 __global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict__ state,
-                                                   long long total, const NbrEntry* __restrict__ table) {
+                                                   long long total, const NbrEntry* __restrict__ table,
+                                                   int faces_only, int depth) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   long long cells = (long long)G.P[0] * G.P[1] * G.P[2];
@@ -28,6 +31,13 @@ __global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict
 #pragma unroll
   for (int d = 0; d < 3; d++) o[d] = (l[d] < 0) ? -1 : (l[d] >= G.nb[d]) ? 1 : 0;
   if (o[0] == 0 && o[1] == 0 && o[2] == 0) return;
+  if (faces_only) {
+    int outside = (o[0] != 0) + (o[1] != 0) + (o[2] != 0);
+    bool deep = false;
+#pragma unroll
+    for (int d = 0; d < 3; d++) deep |= (l[d] < -depth) || (l[d] >= G.nb[d] + depth);
+    if (outside > 1 || deep) return;
+  }
   NbrEntry e = table[slot * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)];
   if (e.src == nullptr) return;  // remote source: written by the halo exchange
   int s[3];
@@ -51,10 +61,10 @@ __global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict
 }
 
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool faces_only) {
   long long total = (long long)nslots * G.P[0] * G.P[1] * G.P[2];
   long long blocks = (total + 255) / 256;
-  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(G, state, total, table);
+  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(G, state, total, table, faces_only ? 1 : 0, 2);
   count_launch();
   return cudaGetLastError();
 }

@@ -65,13 +65,18 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // ------------------------------------------------------------- geometry ----
-template <int NB, int STAGE, int SPLIT>
+// MODE 0 = telescoped step (stage 1 on the box interior+2, U1 in an (n+4)^3
+// scratch, no refill); MODE 1 = per-stage step (both stages
+// on the interior, U1 in a padded (n+8)^3 scratch whose guards are refilled
+// between the stages).
+template <int NB, int STAGE, int SPLIT, int MODE = 0>
 struct Geo {
-  static constexpr int W = (STAGE == 1) ? NB + 4 : NB;       // output columns (and rows) per plane
+  static constexpr int W = (STAGE == 1 && MODE == 0) ? NB + 4 : NB;  // output columns (and rows) per plane
   static constexpr int OFF = (W - NB) / 2;                   // output origin (interior-relative) = -OFF
   static constexpr int K0 = -OFF;                            // first output plane
   static constexpr int NK = W;                               // output planes
-  static constexpr int INO = (STAGE == 1) ? 4 : 2;           // input origin offset (guards / ring)
+  static constexpr int INO = (STAGE == 1 || MODE == 1) ? 4 : 2;  // input origin offset (guards / ring)
+  static constexpr int ORG = INO - 2 - OFF;                  // first staged padded row / plane
   static constexpr int IPX = NB + 2 * INO;                   // padded input row length (= plane rows)
   static constexpr int PLANE = IPX * IPX;                    // doubles per input plane per variable
   static constexpr int NPLANES = NK + 4;                     // input planes streamed
@@ -105,15 +110,19 @@ __host__ __device__ constexpr long long u1_cube() {
   return ((long long)(NB + 4) * (NB + 4) * (NB + 4) * 8 + 255) / 256 * 256 / 8;
 }
 
-template <int NB, int STAGE, int SPLIT>
-__global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLIT>::MINB)
+template <int NB, int STAGE, int SPLIT, int MODE>
+__global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
                        DtRecord* __restrict__ rec, DevStatus* st) {
-  using Gm = Geo<NB, STAGE, SPLIT>;
+  using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
-  constexpr int NT = Gm::NT, H = Gm::H;
-  constexpr long long U1C = u1_cube<NB>();
+  constexpr int NT = Gm::NT, H = Gm::H, ORG = Gm::ORG;
+  // U1 cube stride: (n+4)^3 compact scratch (telescoped) or the padded state layout (per-stage)
+  const long long U1C = (MODE == 0) ? u1_cube<NB>() : G.cube;
+  auto u1_off = [&](int ci, int cj, int k) -> long long {
+    return (MODE == 0) ? ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2) : cell_off(G, ci, cj, k);
+  };
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;                                   // [NS][5][IR][IPX]
   double* Fx = ring + NS * 5 * BAND;                     // [5][H][W+1]
@@ -147,8 +156,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLI
       mbar_expect_tx(&bar[s], 5u * BAND * 8u);
 #pragma unroll
       for (int v = 0; v < 5; v++)
-        bulk_load(ring + (s * 5 + v) * BAND, in + v * in_cube + (long long)p * Gm::PLANE + (long long)jj0 * IPX,
-                  BAND * 8u, &bar[s]);
+        bulk_load(ring + (s * 5 + v) * BAND,
+                  in + v * in_cube + (long long)(p + ORG) * Gm::PLANE + (long long)(jj0 + ORG) * IPX, BAND * 8u,
+                  &bar[s]);
     }
   };
   auto wait_plane = [&](int p) { mbar_wait(&bar[p % NS], (p / NS) & 1); };
@@ -160,7 +170,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLI
       bool fl;
       Prim q = eos(Q[c], Q[BAND + c], Q[2 * BAND + c], Q[3 * BAND + c], Q[4 * BAND + c], G, &fl);
       int r = c / IPX;
-      int x = c - r * IPX - INO, y = jj0 + r - INO;
+      int x = c - r * IPX - INO, y = jj0 + ORG + r - INO;
       // own (non-overlapping) rows of the band only, so each cell counts once
       bool mine = r >= 2 && r < 2 + H;
       if (mine && x >= 0 && x < NB && y >= 0 && y < NB && z >= 0 && z < NB) {
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLI
 #pragma unroll
       for (int v = 0; v < 5; v++) un[v] = __ldg(state + slot * 5 * cube + v * cube + so);
       if (STAGE == 2) {
-        const long long uo = ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2);
+        const long long uo = u1_off(ci, cj, k);
 #pragma unroll
         for (int v = 0; v < 5; v++) v1[v] = __ldg(u1 + slot * 5 * U1C + v * U1C + uo);
       }
@@ -307,7 +317,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLI
         D[v] = (tx + ty) + tz;
       }
       if (STAGE == 1) {
-        double* out = u1 + slot * 5 * U1C + ((long long)(k + 2) * W + (cj + 2)) * W + (ci + 2);
+        double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
 #pragma unroll
         for (int v = 0; v < 5; v++) out[v * U1C] = un[v] - dt * D[v];
       } else {
@@ -334,19 +344,18 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT>::NT, Geo<NB, STAGE, SPLI
     if (tid == 0) { rec[blockIdx.x].s = s_rec; rec[blockIdx.x].g = g_rec; }
   }
 }
-
-template <int NB, int STAGE, int SPLIT>
+template <int NB, int STAGE, int SPLIT, int MODE>
 static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                          const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s) {
-  using Gm = Geo<NB, STAGE, SPLIT>;
+  using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Gm::SMEM);
     attr = true;
   }
-  stage_fused_kernel<NB, STAGE, SPLIT><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, d_dt, h_dt,
-                                                                                records, st);
+  stage_fused_kernel<NB, STAGE, SPLIT, MODE><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, d_dt,
+                                                                                      h_dt, records, st);
   count_launch();
 }
 
@@ -368,13 +377,13 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
     static const int s2v = split_env("ORCHA_SPLIT2", 2);
     s2 = s2v;
-    if (s1 == 4) launch_stage<NB, 1, 4>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<NB, 1, 2>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    if (s2 == 4) launch_stage<NB, 2, 4>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<NB, 2, 2>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (s1 == 4) launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
   } else {
-    launch_stage<NB, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    launch_stage<NB, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
   }
   *nrecords = (long long)nslots * s2;
   return cudaGetLastError();
@@ -383,6 +392,9 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
 cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
                                DevStatus* st, cudaStream_t s);
+cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
+                             const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
+                             long long* nrecords, DevStatus* st, cudaStream_t s);
 
 // The fused path covers 3D blocks of 8^3 and 16^3 with ng = 4 (the paper's
 // "typical block in AMR is 16^3"); other shapes use the reference
@@ -398,6 +410,26 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   if (G.nb[0] == 16) return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+}
+
+// One stage of the per-stage variant (F1): stage 1 -> U1 (padded, interior
+// only; its guards are refilled by orcha_fill_guardcells_stage), stage 2 ->
+// U^{n+1} in place + dt records.
+cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
+                               const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
+                               long long* nrecords, DevStatus* st, cudaStream_t s) {
+  if (!fused_supported(G))
+    return launch_stage_ref(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+  if (G.nb[0] == 16) {
+    if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<16, 2, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (stage == 2) *nrecords = (long long)nslots * 2;
+  } else {
+    if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<8, 2, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (stage == 2) *nrecords = (long long)nslots;
+  }
+  return cudaGetLastError();
 }
 
 }  // namespace orcha

@@ -45,13 +45,15 @@ __device__ __forceinline__ void accumulate_axis(const double* __restrict__ in, l
 // STAGE 1: region = box [-2, n+2) per active axis; U1 = U^n - dt*D(U^n) -> u1.
 // STAGE 2: region = interior; U^{n+1} = 0.5*(U^n + (U1 - dt*D(U1))) -> state,
 //          then the fused dt epilogue (s of U^{n+1}, one record per CTA).
-template <int NDIM, int STAGE>
+// RING = width of the stage-1 ring beyond the interior: 2 for the telescoped
+// step, 0 for the per-stage variant (F1, U1 guards refilled between stages).
+template <int NDIM, int STAGE, int RING = 2>
 __global__ void __launch_bounds__(256) stage_ref_kernel(DevGrid G, double* __restrict__ state,
                                                         double* __restrict__ u1, long long total,
                                                         const SlotInfo* __restrict__ slots,
                                                         const double* __restrict__ d_dt, double h_dt,
                                                         DtRecord* __restrict__ rec, DevStatus* st) {
-  const int w = (STAGE == 1) ? 2 : 0;
+  const int w = (STAGE == 1) ? RING : 0;
   int E[3];
 #pragma unroll
   for (int d = 0; d < 3; d++) E[d] = (d < NDIM) ? G.nb[d] + 2 * w : 1;
@@ -130,6 +132,34 @@ cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int 
   if (G.ndim == 1) return launch_ref<1>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   if (G.ndim == 2) return launch_ref<2>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   return launch_ref<3>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+}
+
+// One stage of the per-stage variant (F1) with the reference kernels:
+// stage 1 on the interior (RING 0) into the padded U1, stage 2 as above.
+template <int NDIM>
+static cudaError_t stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
+                             const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
+                             long long* nrecords, DevStatus* st, cudaStream_t s) {
+  long long c = 1;
+  for (int d = 0; d < NDIM; d++) c *= G.nb[d];
+  long long t = nslots * c;
+  unsigned blocks = (unsigned)((t + 255) / 256);
+  if (stage == 1) {
+    stage_ref_kernel<NDIM, 1, 0><<<blocks, 256, 0, s>>>(G, state, u1, t, slots, d_dt, h_dt, records, st);
+  } else {
+    stage_ref_kernel<NDIM, 2><<<blocks, 256, 0, s>>>(G, state, u1, t, slots, d_dt, h_dt, records, st);
+    *nrecords = blocks;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
+                             const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
+                             long long* nrecords, DevStatus* st, cudaStream_t s) {
+  if (G.ndim == 1) return stage_ref<1>(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+  if (G.ndim == 2) return stage_ref<2>(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+  return stage_ref<3>(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
 }
 
 }  // namespace orcha

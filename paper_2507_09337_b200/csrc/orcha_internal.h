@@ -87,6 +87,9 @@ struct orcha_packet {
   orcha::SlotInfo* d_slots;    // library-owned device table
   bool guards_valid;
   bool records_valid;
+  bool guards_full;            // false after the per-stage (faces, depth 2) fill
+  bool stage1_done;            // per-stage variant: U1 computed, stage 2 pending
+  bool u1_guards_valid;        // per-stage variant: U1 guards refilled
 };
 
 namespace orcha {
@@ -103,7 +106,7 @@ long long records_capacity(const DevGrid& G, long long nslots);
 
 // kernel launchers (kernels_*.cu); all return cudaGetLastError()
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
-                        cudaStream_t s);
+                        cudaStream_t s, bool faces_only = false);
 cudaError_t launch_pack(const DevGrid& G, double* state, const double* staged, int nslots,
                         bool to_state, cudaStream_t s);
 cudaError_t launch_status_reset(DevStatus* st, cudaStream_t s);

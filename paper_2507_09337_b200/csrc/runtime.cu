@@ -57,6 +57,12 @@ cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int 
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
                                  DevStatus* st, cudaStream_t s);
+cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
+                             const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
+                             long long* nrecords, DevStatus* st, cudaStream_t s);
+cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
+                               const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
+                               long long* nrecords, DevStatus* st, cudaStream_t s);
 }  // namespace orcha
 
 extern "C" const char* orcha_last_error(void) { return g_last_error.c_str(); }
@@ -154,6 +160,7 @@ extern "C" int32_t orcha_packet_bytes(const orcha_grid* g, int32_t n, size_t* sb
 struct FillPlan {
   std::vector<orcha_packet*> packets;
   std::vector<NbrEntry*> d_tables;   // one per packet (library-owned device memory)
+  std::vector<NbrEntry*> d_tables_u1;  // same, sources in the stage-1 buffers (per-stage variant)
   CommPlan* remote = nullptr;        // guard cells sourced from other ranks (comm.cu)
   bool has_remote = false;
 };
@@ -168,6 +175,7 @@ static void drop_plans_with(orcha_packet* p) {
     for (auto* q : f->packets) hit |= (q == p);
     if (hit) {
       for (auto* t : f->d_tables) cudaFree(t);
+      for (auto* t : f->d_tables_u1) cudaFree(t);
       comm_free_plan(f->remote);
       delete f;
       g_plans.erase(g_plans.begin() + i);
@@ -204,6 +212,8 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
   p->nrecords = 0;
   p->guards_valid = false;
   p->records_valid = false;
+  p->stage1_done = false;
+  p->u1_guards_valid = false;
   std::vector<SlotInfo> si(n);
   const DevGrid& G = g->dev;
   for (int s = 0; s < n; s++) {
@@ -260,6 +270,8 @@ static int32_t pack_impl(orcha_packet* p, const double* src, cudaMemcpyKind kind
   if (e != cudaSuccess) return cuda_fail(e, "pack kernel");
   p->guards_valid = false;
   p->records_valid = false;
+  p->stage1_done = false;       // the staging area overwrote the stage-1 buffer
+  p->u1_guards_valid = false;
   return ORCHA_OK;
 }
 
@@ -381,6 +393,7 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
             if (it == where.end()) {
               if (!comm) {
                 for (auto* t : f->d_tables) cudaFree(t);
+                for (auto* t : f->d_tables_u1) cudaFree(t);
                 delete f;
                 return fail(ORCHA_E_RANGE, "neighbour block " + std::to_string(h.src_block) +
                                                " is not resident on this device and no communicator was given");
@@ -393,15 +406,35 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
             }
           }
     }
+    // the same table for the stage-1 buffer (per-stage variant): sources in
+    // each source packet's scratch, which has the state's padded layout
+    std::vector<NbrEntry> tab1 = tab;
+    for (auto& e : tab1)
+      if (e.src) {
+        for (int q2 = 0; q2 < npk; q2++) {
+          orcha_packet* sp = pk[q2];
+          if (e.src >= sp->state && e.src < sp->state + (long long)sp->nslots * kNVar * G.cube) {
+            e.src = sp->scratch + (e.src - sp->state);
+            break;
+          }
+        }
+      }
     NbrEntry* d = nullptr;
+    NbrEntry* d1 = nullptr;
     cudaError_t err = cudaMalloc(&d, tab.size() * sizeof(NbrEntry));
     if (err == cudaSuccess) err = cudaMemcpy(d, tab.data(), tab.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&d1, tab1.size() * sizeof(NbrEntry));
+    if (err == cudaSuccess) err = cudaMemcpy(d1, tab1.data(), tab1.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
     if (err != cudaSuccess) {
       for (auto* t : f->d_tables) cudaFree(t);
+      for (auto* t : f->d_tables_u1) cudaFree(t);
+      cudaFree(d);
+      cudaFree(d1);
       delete f;
       return cuda_fail(err, "upload neighbour table");
     }
     f->d_tables.push_back(d);
+    f->d_tables_u1.push_back(d1);
   }
   *out = f;
   return ORCHA_OK;
@@ -423,26 +456,49 @@ static int32_t get_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fill
   return ORCHA_OK;
 }
 
-extern "C" int32_t orcha_fill_guardcells(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, void* stream) {
+static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer, bool faces_only,
+                         void* stream) {
   if (!pk || npk < 1) return fail(ORCHA_E_ARG, "no packets");
-  for (int q = 0; q < npk; q++)
+  if (buffer != 0 && buffer != 1) return fail(ORCHA_E_ARG, "buffer must be 0 (state) or 1 (stage-1 state)");
+  for (int q = 0; q < npk; q++) {
     if (!pk[q]) return fail(ORCHA_E_ARG, "null packet");
+    if (buffer == 1 && !pk[q]->stage1_done)
+      return fail(ORCHA_E_STATE, "stage-1 buffer refill requires orcha_hydro_stage(packet, 1, ...) first");
+  }
   FillPlan* f = nullptr;
   int32_t rc = get_plan(pk, npk, comm, &f);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (f->has_remote) {
-    CommPlan* cp = nullptr;  // cached by the communicator per packet set
-    rc = comm_build_plan(comm, pk, npk, &cp);
+    CommPlan* cp = nullptr;  // cached by the communicator per packet set and buffer
+    rc = comm_build_plan(comm, pk, npk, buffer, &cp);
     if (rc == ORCHA_OK) rc = comm_exchange(comm, cp, s);
     if (rc) return rc;
   }
   for (int q = 0; q < npk; q++) {
-    cudaError_t e = launch_fill(pk[q]->grid->dev, pk[q]->state, pk[q]->nslots, f->d_tables[q], s);
+    double* dst = buffer ? pk[q]->scratch : pk[q]->state;
+    const NbrEntry* tab = buffer ? f->d_tables_u1[q] : f->d_tables[q];
+    cudaError_t e = launch_fill(pk[q]->grid->dev, dst, pk[q]->nslots, tab, s, faces_only);
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   }
-  for (int q = 0; q < npk; q++) pk[q]->guards_valid = true;
+  for (int q = 0; q < npk; q++) {
+    if (buffer) {
+      pk[q]->u1_guards_valid = true;
+    } else {
+      pk[q]->guards_valid = true;
+      pk[q]->guards_full = !faces_only;
+    }
+  }
   return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_fill_guardcells(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, void* stream) {
+  return fill_impl(pk, npk, comm, 0, false, stream);
+}
+
+extern "C" int32_t orcha_fill_guardcells_stage(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
+                                               int32_t buffer, void* stream) {
+  return fill_impl(pk, npk, comm, buffer, true, stream);
 }
 
 // --------------------------------------------------------------- dt ------
@@ -495,8 +551,9 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
 // ----------------------------------------------------------- advance -----
 static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, void* stream) {
   if (!p) return fail(ORCHA_E_ARG, "null packet");
-  if (!p->guards_valid)
-    return fail(ORCHA_E_STATE, "orcha_fill_guardcells must precede every orcha_hydro_advance (guards are stale)");
+  if (!p->guards_valid || !p->guards_full)
+    return fail(ORCHA_E_STATE, "orcha_fill_guardcells must precede every orcha_hydro_advance (guards are stale, "
+                               "or only the per-stage fill ran)");
   cudaStream_t s = (cudaStream_t)stream;
   const DevGrid& G = p->grid->dev;
   cudaError_t e;
@@ -510,6 +567,8 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   p->guards_valid = false;
   p->records_valid = true;
+  p->stage1_done = false;
+  p->u1_guards_valid = false;
   return ORCHA_OK;
 }
 
@@ -519,4 +578,43 @@ extern "C" int32_t orcha_hydro_advance(orcha_packet* p, double dt, void* stream)
 extern "C" int32_t orcha_hydro_advance_devdt(orcha_packet* p, const double* d_dt, void* stream) {
   if (!d_dt) return fail(ORCHA_E_ARG, "null d_dt");
   return advance_impl(p, d_dt, 0.0, stream);
+}
+
+// ------------------------------------------- per-stage variant (F1) ------
+static int32_t stage_impl(orcha_packet* p, int32_t stage, const double* d_dt, double h_dt, void* stream) {
+  if (!p) return fail(ORCHA_E_ARG, "null packet");
+  if (stage != 1 && stage != 2) return fail(ORCHA_E_ARG, "stage must be 1 or 2");
+  if (stage == 1 && !p->guards_valid)
+    return fail(ORCHA_E_STATE, "stage 1 needs a guard fill of the state since the last pack/advance");
+  if (stage == 2 && !(p->stage1_done && p->u1_guards_valid))
+    return fail(ORCHA_E_STATE, "stage 2 needs stage 1 and a guard refill of the stage-1 buffer (buffer 1)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevGrid& G = p->grid->dev;
+  cudaError_t e;
+  if (kernel_variant() == 0)
+    e = launch_stage_ref(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
+                         &p->nrecords, p->status, s);
+  else
+    e = launch_stage_fused(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
+                           &p->nrecords, p->status, s);
+  if (e != cudaSuccess) return cuda_fail(e, "stage kernels");
+  if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
+  if (stage == 1) {
+    p->stage1_done = true;
+    p->u1_guards_valid = false;
+  } else {
+    p->stage1_done = false;
+    p->u1_guards_valid = false;
+    p->guards_valid = false;
+    p->records_valid = true;
+  }
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_hydro_stage(orcha_packet* p, int32_t stage, double dt, void* stream) {
+  return stage_impl(p, stage, nullptr, dt, stream);
+}
+extern "C" int32_t orcha_hydro_stage_devdt(orcha_packet* p, int32_t stage, const double* d_dt, void* stream) {
+  if (!d_dt) return fail(ORCHA_E_ARG, "null d_dt");
+  return stage_impl(p, stage, d_dt, 0.0, stream);
 }

@@ -176,9 +176,9 @@ class Comm:
                  owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), hs)
         return [Comm(grid, ctypes.c_void_p(hs[r]), nranks, r, owner) for r in range(nranks)]
 
-    def push(self, packets, stream=None):
+    def push(self, packets, stream=None, buffer: int = 0):
         arr, n = _handles(packets)
-        abi.call(self.lib, "orcha_comm_push", self.handle, arr, n, ctypes.c_void_p(_stream_ptr(stream)))
+        abi.call(self.lib, "orcha_comm_push", self.handle, arr, n, int(buffer), ctypes.c_void_p(_stream_ptr(stream)))
 
     def destroy(self):
         if self.handle:
@@ -235,17 +235,49 @@ def set_kernel_variant(lib, v: int):
     abi.call(lib, "orcha_set_kernel_variant", int(v))
 
 
-def run(packets, nsteps: Optional[int] = None, t_end: float = math.inf, comm=None, stream=None):
-    """The driver loop of SURVEY 8(c): fill -> dt (then t_end clamp) -> advance,
+def orcha_hydro_stage(packet: Packet, stage: int, dt: float, stream=None):
+    abi.call(packet.lib, "orcha_hydro_stage", packet.handle, int(stage), float(dt),
+             ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def orcha_fill_guardcells_stage(packets, buffer: int, comm=None, stream=None):
+    arr, n = _handles(packets)
+    abi.call(packets[0].lib, "orcha_fill_guardcells_stage", arr, n, comm.handle if comm is not None else None,
+             int(buffer), ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def step(packets, dt: float, comm=None, stream=None, method: str = "telescoped"):
+    """One RK2 step after the state's guard fill: telescoped (the paper's
+    communication-avoiding step) or per-stage (F1: refill U1's
+    guards between the stages)."""
+    if method == "telescoped":
+        for p in packets:
+            orcha_hydro_advance(p, dt, stream)
+    elif method == "per-stage":
+        # the caller's state fill may be the full one or the per-stage one
+        for p in packets:
+            orcha_hydro_stage(p, 1, dt, stream)
+        orcha_fill_guardcells_stage(packets, 1, comm, stream)
+        for p in packets:
+            orcha_hydro_stage(p, 2, dt, stream)
+    else:
+        raise ValueError(method)
+
+
+def run(packets, nsteps: Optional[int] = None, t_end: float = math.inf, comm=None, stream=None,
+        method: str = "telescoped"):
+    """The driver loop of SURVEY 8(c): fill -> dt (then t_end clamp) -> step,
     every call through the C ABI.  Returns (t, steps, [dt_info...])."""
     t = 0.0
     log = []
     n = 0
     while (nsteps is None or n < nsteps) and t < t_end:
-        orcha_fill_guardcells(packets, comm, stream)
+        if method == "per-stage":
+            orcha_fill_guardcells_stage(packets, 0, comm, stream)
+        else:
+            orcha_fill_guardcells(packets, comm, stream)
         info = orcha_compute_dt(packets, t_end - t, comm, stream)
-        for p in packets:
-            orcha_hydro_advance(p, info.dt, stream)
+        step(packets, info.dt, comm, stream, method)
         t = t + info.dt
         n += 1
         log.append((info.dt, info.smax, info.argmax, info.tag))

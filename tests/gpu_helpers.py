@@ -48,16 +48,16 @@ def gather(g, pk):
     return out
 
 
-def gpu_run(g, U0, nsteps=None, t_end=math.inf, npackets=1, shuffle=False):
+def gpu_run(g, U0, nsteps=None, t_end=math.inf, npackets=1, shuffle=False, method="telescoped"):
     from paper_2507_09337_b200 import hydro
     pk = gpu_setup(g, U0, npackets, shuffle)
-    t, n, log = hydro.run(pk, nsteps=nsteps, t_end=t_end)
+    t, n, log = hydro.run(pk, nsteps=nsteps, t_end=t_end, method=method)
     return gather(g, pk), t, log, pk
 
 
-def oracle_run(og, U0, nsteps=None, t_end=math.inf):
+def oracle_run(og, U0, nsteps=None, t_end=math.inf, mode="telescoped"):
     U = oracle.padded(og, U0)
-    log = oracle.run(og, U, nsteps=nsteps, t_end=t_end)
+    log = oracle.run(og, U, nsteps=nsteps, t_end=t_end, mode=mode)
     return U[og.interior].copy(), log
 
 

@@ -92,7 +92,7 @@ struct Geo {
   // warp count is chosen so every warp gets two slots (two rounds)
   static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
   static constexpr int NSLOT = SX + SY + SZ;
-  static constexpr int NW = (NB == 16) ? (NSLOT + 1) / 2 : (W * W + 31) / 32;
+  static constexpr int NW = (NB >= 16) ? (NSLOT + 1) / 2 : (W * W + 31) / 32;
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   static constexpr size_t SMEM = sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64;
@@ -381,6 +381,10 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
     else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+  } else if constexpr (NB == 32) {
+    launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    s2 = 4;
   } else {
     launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
@@ -396,11 +400,13 @@ cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double*
                              const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                              long long* nrecords, DevStatus* st, cudaStream_t s);
 
-// The fused path covers 3D blocks of 8^3 and 16^3 with ng = 4 (the paper's
-// "typical block in AMR is 16^3"); other shapes use the reference
-// kernels (same results).
+// The fused path covers 3D blocks of 8^3, 16^3 and 32^3 with ng = 4 (the
+// paper's "typical block in AMR is 16^3"; BASELINE configs[4]
+// sweeps 8^3 / 16^3 / 32^3); other shapes use the reference kernels (same
+// results).
 bool fused_supported(const DevGrid& G) {
-  return G.ndim == 3 && G.ng == 4 && G.nb[0] == G.nb[1] && G.nb[1] == G.nb[2] && (G.nb[0] == 16 || G.nb[0] == 8);
+  return G.ndim == 3 && G.ng == 4 && G.nb[0] == G.nb[1] && G.nb[1] == G.nb[2] &&
+         (G.nb[0] == 16 || G.nb[0] == 8 || G.nb[0] == 32);
 }
 
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
@@ -409,6 +415,7 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   if (G.nb[0] == 16) return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+  if (G.nb[0] == 32) return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
 }
 
@@ -424,6 +431,10 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
     if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     else launch_stage<16, 2, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     if (stage == 2) *nrecords = (long long)nslots * 2;
+  } else if (G.nb[0] == 32) {
+    if (stage == 1) launch_stage<32, 1, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    else launch_stage<32, 2, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (stage == 2) *nrecords = (long long)nslots * 4;
   } else {
     if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     else launch_stage<8, 2, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);

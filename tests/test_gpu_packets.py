@@ -1,0 +1,58 @@
+"""BASELINE.json configs[4] as a parity case: the same global 3D Sedov grid
+decomposed into 8^3, 16^3 or 32^3 blocks and split into packets of 8 ... all
+blocks (sec 4.3: "n is provided by the users at runtime") gives
+the oracle's global result bitwise (parity build) for every block size and
+packet size, and bitwise-identical results across packet sizes in the
+production build (determinism across packet sizes)."""
+import numpy as np
+import pytest
+
+import orcha_inputs as inp
+from tests import gpu_helpers as H
+
+pytestmark = pytest.mark.gpu
+N = (64, 64, 64)
+STEPS = 4
+
+
+@pytest.fixture(scope="module")
+def oracle_ref():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    g = H.make_grid(3, (16, 16, 16), (4, 4, 4))
+    return H.oracle_run(H.oracle_grid(g), inp.sedov(N), nsteps=STEPS)
+
+
+def _run(nb, packet_size, parity):
+    from paper_2507_09337_b200 import hydro
+    nblk = tuple(n // nb for n in N)
+    g = H.make_grid(3, (nb,) * 3, nblk, parity=parity)
+    ids = np.random.default_rng(nb + packet_size).permutation(g.nblocks)
+    parts = [ids[i:i + packet_size] for i in range(0, len(ids), packet_size)]
+    pk = [hydro.Packet(g, p) for p in parts]
+    for p in pk:
+        p.pack(inp.sedov_packet(N, (nb,) * 3, p.block_ids))
+    t, n, log = hydro.run(pk, nsteps=STEPS)
+    return H.gather(g, pk), log
+
+
+@pytest.mark.parametrize("nb,packet_size", [(8, 8), (8, 64), (8, 512), (16, 8), (16, 64), (32, 8)])
+def test_packet_sweep_parity_build_bitwise(oracle_ref, nb, packet_size):
+    O, olog = oracle_ref
+    G, log = _run(nb, packet_size, True)
+    assert [x[0] for x in log] == olog.dts
+    assert np.array_equal(G, O)
+
+
+@pytest.mark.parametrize("nb", [8, 16, 32])
+def test_packet_sizes_bitwise_identical_production(oracle_ref, nb):
+    O, _ = oracle_ref
+    nblocks = (64 // nb) ** 3
+    ref, _ = _run(nb, nblocks, False)
+    assert H.parity_error(ref, O) <= 1e-12
+    for ps in (8, max(8, nblocks // 3)):
+        if ps >= nblocks:
+            continue
+        G, _ = _run(nb, ps, False)
+        assert np.array_equal(G, ref)

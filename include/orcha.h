@@ -240,6 +240,16 @@ int64_t orcha_launch_count(void);
 int32_t orcha_set_kernel_variant(int32_t variant);
 int32_t orcha_get_kernel_variant(void);
 
+/* Guard push (default OFF -- measured slower than the gather fill on B200,
+ * DESIGN.md 6; ORCHA_PUSH=1 in the environment turns it on at load): the
+ * fused kernels that produce a new state also scatter each new
+ * interior cell into every guard cell of a resident block whose ghost-fill
+ * source it is (the inverse of the gather fill's per-axis images, so the
+ * guard values are bitwise the same).  The next orcha_fill_guardcells* call
+ * with the same packet set then only runs the cross-rank exchange.  Turning it
+ * off makes every fill gather.  Always returns ORCHA_OK. */
+int32_t orcha_set_guard_push(int32_t on);
+
 const char* orcha_last_error(void);
 
 /* ------------------------------------------------------- multi-GPU ------ */

@@ -30,6 +30,7 @@
 
 #include "hydro_math.cuh"
 #include "orcha_internal.h"
+#include "push.cuh"
 #include "reduce.cuh"
 
 namespace orcha {
@@ -110,11 +111,11 @@ __host__ __device__ constexpr long long u1_cube() {
   return ((long long)(NB + 4) * (NB + 4) * (NB + 4) * 8 + 255) / 256 * 256 / 8;
 }
 
-template <int NB, int STAGE, int SPLIT, int MODE>
+template <int NB, int STAGE, int SPLIT, int MODE, bool PUSH>
 __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
-                       DtRecord* __restrict__ rec, DevStatus* st) {
+                       DtRecord* __restrict__ rec, DevStatus* st, const PushEntry* __restrict__ push) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
   constexpr int NT = Gm::NT, H = Gm::H, ORG = Gm::ORG;
@@ -320,6 +321,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
 #pragma unroll
         for (int v = 0; v < 5; v++) out[v * U1C] = un[v] - dt * D[v];
+        if (MODE == 1 && PUSH) {  // per-stage: scatter U1 into the U1 guards of the neighbours
+          double w[5];
+#pragma unroll
+          for (int v = 0; v < 5; v++) w[v] = un[v] - dt * D[v];
+          push_cell(G, push + slot * 27, ci, cj, k, w);
+        }
       } else {
         double nw[5];
 #pragma unroll
@@ -327,6 +334,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         double* dst = state + slot * 5 * cube + so;
 #pragma unroll
         for (int v = 0; v < 5; v++) dst[v * cube] = nw[v];
+        if (PUSH) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
         bool f2;
         Prim q = eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
         double s = signal_speed<3>(q, G);
@@ -346,16 +354,25 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 }
 template <int NB, int STAGE, int SPLIT, int MODE>
 static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
-                         const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s) {
+                         const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s,
+                         const PushEntry* push = nullptr) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Gm::SMEM);
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
     attr = true;
   }
-  stage_fused_kernel<NB, STAGE, SPLIT, MODE><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, d_dt,
-                                                                                      h_dt, records, st);
+  // the guard-push epilogue is a separate instantiation so the default
+  // kernels carry none of its register pressure
+  if (push)
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, true><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, push);
+  else
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, false><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, nullptr);
   count_launch();
 }
 
@@ -371,7 +388,7 @@ static int split_env(const char* name, int dflt) {
 template <int NB>
 static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
-                             cudaStream_t s) {
+                             cudaStream_t s, const PushEntry* push) {
   int s2 = 1;
   if constexpr (NB == 16) {
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
@@ -379,15 +396,15 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
     s2 = s2v;
     if (s1 == 4) launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
     else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
   } else if constexpr (NB == 32) {
     launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     s2 = 4;
   } else {
     launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
   }
   *nrecords = (long long)nslots * s2;
   return cudaGetLastError();
@@ -403,41 +420,45 @@ cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double*
 // The fused path covers 3D blocks of 8^3, 16^3 and 32^3 with ng = 4 (the
 // paper's "typical block in AMR is 16^3"; BASELINE configs[4]
 // sweeps 8^3 / 16^3 / 32^3); other shapes use the reference kernels (same
-// results).
+// results, no guard push).
 bool fused_supported(const DevGrid& G) {
   return G.ndim == 3 && G.ng == 4 && G.nb[0] == G.nb[1] && G.nb[1] == G.nb[2] &&
          (G.nb[0] == 16 || G.nb[0] == 8 || G.nb[0] == 32);
 }
 
+// `push` (optional): the per-slot push tables of the packet's state; when
+// given, stage 2 also scatters U^{n+1} into the guards of the resident blocks
+// (push.cuh), which makes the next gather fill unnecessary.
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
-                                 DevStatus* st, cudaStream_t s) {
+                                 DevStatus* st, cudaStream_t s, const PushEntry* push) {
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  if (G.nb[0] == 16) return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  if (G.nb[0] == 32) return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+  if (G.nb[0] == 16) return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push);
+  if (G.nb[0] == 32) return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push);
+  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push);
 }
 
 // One stage of the per-stage variant (F1): stage 1 -> U1 (padded, interior
-// only; its guards are refilled by orcha_fill_guardcells_stage), stage 2 ->
-// U^{n+1} in place + dt records.
+// only), stage 2 -> U^{n+1} in place + dt records.  `push` (optional): the
+// push tables of the buffer this stage writes (stage 1: the stage-1 buffers,
+// stage 2: the states).
 cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
-                               long long* nrecords, DevStatus* st, cudaStream_t s) {
+                               long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push) {
   if (!fused_supported(G))
     return launch_stage_ref(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   if (G.nb[0] == 16) {
-    if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<16, 2, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    else launch_stage<16, 2, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     if (stage == 2) *nrecords = (long long)nslots * 2;
   } else if (G.nb[0] == 32) {
-    if (stage == 1) launch_stage<32, 1, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<32, 2, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (stage == 1) launch_stage<32, 1, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    else launch_stage<32, 2, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     if (stage == 2) *nrecords = (long long)nslots * 4;
   } else {
-    if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<8, 2, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    else launch_stage<8, 2, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     if (stage == 2) *nrecords = (long long)nslots;
   }
   return cudaGetLastError();

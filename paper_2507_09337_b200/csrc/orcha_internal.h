@@ -39,6 +39,17 @@ struct NbrEntry {
   int32_t flip;        // bit (1+d) set -> negate variable 1+d (reflect on axis d)
 };
 
+// Push table: one entry per (slot, direction o): the block whose guards in
+// direction -o (seen from it) are sourced by this block's cells -- the block
+// at b+o (periodic wrap), or b itself along axes where b+o leaves the domain
+// through a clamp / mirror boundary.  Per-axis modes as NbrEntry (shift,
+// clamp, mirror); nullptr = target not resident (remote: exchange fills it).
+struct PushEntry {
+  double* dst;         // base of the target block's var-0 cube (state or stage-1 buffer)
+  int32_t mode;        // 2 bits per axis
+  int32_t flip;        // bit (1+d): negate variable 1+d
+};
+
 // Sticky per-packet status word (lives in the scratch tail).
 struct DevStatus {
   unsigned long long first_bad;   // lowest global cell index with a non-physical state (ULLONG_MAX = none)
@@ -90,6 +101,12 @@ struct orcha_packet {
   bool guards_full;            // false after the per-stage (faces, depth 2) fill
   bool stage1_done;            // per-stage variant: U1 computed, stage 2 pending
   bool u1_guards_valid;        // per-stage variant: U1 guards refilled
+  // guard push (push.cuh): tables of the last fill plan this packet was filled with
+  const orcha::PushEntry* d_push;     // targets in the states
+  const orcha::PushEntry* d_push_u1;  // targets in the stage-1 buffers
+  const FillPlan* push_plan;          // the plan those tables belong to
+  bool guards_pushed;          // the last state update scattered itself into the guards (push_plan)
+  bool u1_pushed;              // same for the stage-1 buffer
 };
 
 namespace orcha {

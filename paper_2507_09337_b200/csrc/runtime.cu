@@ -56,14 +56,31 @@ cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int 
                                DevStatus* st, cudaStream_t s);
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
-                                 DevStatus* st, cudaStream_t s);
+                                 DevStatus* st, cudaStream_t s, const PushEntry* push);
 cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                              const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                              long long* nrecords, DevStatus* st, cudaStream_t s);
 cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
-                               long long* nrecords, DevStatus* st, cudaStream_t s);
+                               long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push);
+bool fused_supported(const DevGrid& G);
 }  // namespace orcha
+
+// Guard push on/off.  Default OFF: measured on cfg4 the per-cell scatter in
+// the stage-2 epilogue costs more (+1.0 ms) than the gather fill it removes
+// (0.73 ms); ORCHA_PUSH=1 (or orcha_set_guard_push(1)) turns it on.
+static int g_push = -1;
+static bool push_enabled() {
+  if (g_push < 0) {
+    const char* e = getenv("ORCHA_PUSH");
+    g_push = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_push == 1;
+}
+extern "C" int32_t orcha_set_guard_push(int32_t on) {
+  g_push = on ? 1 : 0;
+  return ORCHA_OK;
+}
 
 extern "C" const char* orcha_last_error(void) { return g_last_error.c_str(); }
 extern "C" int64_t orcha_launch_count(void) { return g_launches.load(); }
@@ -161,6 +178,10 @@ struct FillPlan {
   std::vector<orcha_packet*> packets;
   std::vector<NbrEntry*> d_tables;   // one per packet (library-owned device memory)
   std::vector<NbrEntry*> d_tables_u1;  // same, sources in the stage-1 buffers (per-stage variant)
+  std::vector<PushEntry*> d_push;      // push tables (targets in the states), one per packet
+  std::vector<PushEntry*> d_push_u1;   // push tables (targets in the stage-1 buffers)
+  std::vector<NbrEntry*> d_cross;      // gather tables of the cross-packet directions only (or null)
+  std::vector<NbrEntry*> d_cross_u1;
   CommPlan* remote = nullptr;        // guard cells sourced from other ranks (comm.cu)
   bool has_remote = false;
 };
@@ -176,6 +197,12 @@ static void drop_plans_with(orcha_packet* p) {
     if (hit) {
       for (auto* t : f->d_tables) cudaFree(t);
       for (auto* t : f->d_tables_u1) cudaFree(t);
+      for (auto* t : f->d_push) cudaFree(t);
+      for (auto* t : f->d_push_u1) cudaFree(t);
+      for (auto* t : f->d_cross) cudaFree(t);
+      for (auto* t : f->d_cross_u1) cudaFree(t);
+      for (auto* q : f->packets)
+        if (q->push_plan == f) { q->push_plan = nullptr; q->d_push = q->d_push_u1 = nullptr; }
       comm_free_plan(f->remote);
       delete f;
       g_plans.erase(g_plans.begin() + i);
@@ -214,6 +241,9 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
   p->records_valid = false;
   p->stage1_done = false;
   p->u1_guards_valid = false;
+  p->d_push = p->d_push_u1 = nullptr;
+  p->push_plan = nullptr;
+  p->guards_pushed = p->u1_pushed = false;
   std::vector<SlotInfo> si(n);
   const DevGrid& G = g->dev;
   for (int s = 0; s < n; s++) {
@@ -272,6 +302,7 @@ static int32_t pack_impl(orcha_packet* p, const double* src, cudaMemcpyKind kind
   p->records_valid = false;
   p->stage1_done = false;       // the staging area overwrote the stage-1 buffer
   p->u1_guards_valid = false;
+  p->guards_pushed = p->u1_pushed = false;  // new interior, not scattered into any guards
   return ORCHA_OK;
 }
 
@@ -435,6 +466,83 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     }
     f->d_tables.push_back(d);
     f->d_tables_u1.push_back(d1);
+    // push tables: target of direction o = make_entry(b, o).src_block (the
+    // neighbour at b+o, or b itself across a clamp/mirror boundary)
+    std::vector<PushEntry> pt((size_t)p->nslots * 27), pt1;
+    for (int s = 0; s < p->nslots; s++) {
+      long long b = p->ids[s];
+      int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
+                   (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+      for (int dd = 0; dd < 27; dd++) {
+        int o[3] = {dd % 3 - 1, (dd / 3) % 3 - 1, dd / 9 - 1};
+        PushEntry& e = pt[(size_t)s * 27 + dd];
+        bool valid = true;
+        for (int a = g->desc.ndim; a < 3; a++) valid &= (o[a] == 0);
+        if (!valid) { e.dst = nullptr; e.mode = 0; e.flip = 0; continue; }
+        HostEntry h = make_entry(g, bc, o);
+        e.mode = h.mode;
+        e.flip = h.flip;
+        // same packet only: a push into another packet's guards would land
+        // before that packet's own advance has read them (stage 1)
+        auto it = where.find(h.src_block);
+        e.dst = (it == where.end() || it->second.first != q)
+                    ? nullptr
+                    : pk[it->second.first]->state + (long long)it->second.second * kNVar * G.cube;
+      }
+    }
+    pt1 = pt;
+    for (auto& e : pt1)
+      if (e.dst)
+        for (int q2 = 0; q2 < npk; q2++) {
+          orcha_packet* sp = pk[q2];
+          if (e.dst >= sp->state && e.dst < sp->state + (long long)sp->nslots * kNVar * G.cube) {
+            e.dst = sp->scratch + (e.dst - sp->state);
+            break;
+          }
+        }
+    PushEntry* dp = nullptr;
+    PushEntry* dp1 = nullptr;
+    err = cudaMalloc(&dp, pt.size() * sizeof(PushEntry));
+    if (err == cudaSuccess) err = cudaMemcpy(dp, pt.data(), pt.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&dp1, pt1.size() * sizeof(PushEntry));
+    if (err == cudaSuccess) err = cudaMemcpy(dp1, pt1.data(), pt1.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) return cuda_fail(err, "upload push table");  // (tables freed with the plan)
+    f->d_push.push_back(dp);
+    f->d_push_u1.push_back(dp1);
+    // cross-packet gather tables: only the directions whose source block lives
+    // in another resident packet (the pushes cover the same-packet ones)
+    std::vector<NbrEntry> xc = tab, xc1 = tab1;
+    bool any_cross = false;
+    for (int s = 0; s < p->nslots; s++) {
+      long long b = p->ids[s];
+      int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
+                   (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+      for (int dd = 0; dd < 27; dd++) {
+        size_t i = (size_t)s * 27 + dd;
+        if (!xc[i].src) continue;
+        int o[3] = {dd % 3 - 1, (dd / 3) % 3 - 1, dd / 9 - 1};
+        bool valid = true;
+        for (int a = g->desc.ndim; a < 3; a++) valid &= (o[a] == 0);
+        auto it = valid ? where.find(make_entry(g, bc, o).src_block) : where.end();
+        if (!valid || it == where.end() || it->second.first == q) {
+          xc[i].src = nullptr;
+          xc1[i].src = nullptr;
+        } else {
+          any_cross = true;
+        }
+      }
+    }
+    NbrEntry* dx = nullptr;
+    NbrEntry* dx1 = nullptr;
+    if (any_cross) {
+      err = cudaMalloc(&dx, xc.size() * sizeof(NbrEntry));
+      if (err == cudaSuccess) err = cudaMemcpy(dx, xc.data(), xc.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
+      if (err == cudaSuccess) err = cudaMalloc(&dx1, xc1.size() * sizeof(NbrEntry));
+      if (err == cudaSuccess) err = cudaMemcpy(dx1, xc1.data(), xc1.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
+      if (err != cudaSuccess) return cuda_fail(err, "upload cross-packet table");
+    }
+    f->d_cross.push_back(dx);
+    f->d_cross_u1.push_back(dx1);
   }
   *out = f;
   return ORCHA_OK;
@@ -475,18 +583,30 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
     if (rc == ORCHA_OK) rc = comm_exchange(comm, cp, s);
     if (rc) return rc;
   }
+  // If every packet's last update of this buffer scattered itself into the
+  // guards with this plan's push tables (push.cuh), the local guards are
+  // already current: only the exchange above was needed.
+  bool all_pushed = push_enabled();
+  for (int q = 0; q < npk; q++)
+    all_pushed &= pk[q]->push_plan == f && (buffer ? pk[q]->u1_pushed : pk[q]->guards_pushed);
   for (int q = 0; q < npk; q++) {
     double* dst = buffer ? pk[q]->scratch : pk[q]->state;
-    const NbrEntry* tab = buffer ? f->d_tables_u1[q] : f->d_tables[q];
+    const NbrEntry* tab = all_pushed ? (buffer ? f->d_cross_u1[q] : f->d_cross[q])   // cross-packet only
+                                     : (buffer ? f->d_tables_u1[q] : f->d_tables[q]);
+    if (!tab) continue;  // pushed, and no source in another packet
     cudaError_t e = launch_fill(pk[q]->grid->dev, dst, pk[q]->nslots, tab, s, faces_only);
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   }
   for (int q = 0; q < npk; q++) {
+    pk[q]->d_push = f->d_push[q];
+    pk[q]->d_push_u1 = f->d_push_u1[q];
+    pk[q]->push_plan = f;
     if (buffer) {
       pk[q]->u1_guards_valid = true;
     } else {
       pk[q]->guards_valid = true;
-      pk[q]->guards_full = !faces_only;
+      // a push writes every same-packet guard; cross-packet ones are full unless faces-only
+      pk[q]->guards_full = !faces_only || (all_pushed && f->d_cross[q] == nullptr);
     }
   }
   return ORCHA_OK;
@@ -557,18 +677,22 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   cudaStream_t s = (cudaStream_t)stream;
   const DevGrid& G = p->grid->dev;
   cudaError_t e;
-  if (kernel_variant() == 0)
+  const bool fused = kernel_variant() == 1;
+  const PushEntry* push = (fused && push_enabled() && fused_supported(G) && p->push_plan) ? p->d_push : nullptr;
+  if (!fused)
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
   else
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                             &p->nrecords, p->status, s);
+                             &p->nrecords, p->status, s, push);
   if (e != cudaSuccess) return cuda_fail(e, "advance kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   p->guards_valid = false;
+  p->guards_pushed = push != nullptr;
   p->records_valid = true;
   p->stage1_done = false;
   p->u1_guards_valid = false;
+  p->u1_pushed = false;
   return ORCHA_OK;
 }
 
@@ -591,21 +715,27 @@ static int32_t stage_impl(orcha_packet* p, int32_t stage, const double* d_dt, do
   cudaStream_t s = (cudaStream_t)stream;
   const DevGrid& G = p->grid->dev;
   cudaError_t e;
-  if (kernel_variant() == 0)
+  const bool fused = kernel_variant() == 1;
+  const PushEntry* push = nullptr;
+  if (fused && push_enabled() && fused_supported(G) && p->push_plan) push = (stage == 1) ? p->d_push_u1 : p->d_push;
+  if (!fused)
     e = launch_stage_ref(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                          &p->nrecords, p->status, s);
   else
     e = launch_stage_fused(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                           &p->nrecords, p->status, s);
+                           &p->nrecords, p->status, s, push);
   if (e != cudaSuccess) return cuda_fail(e, "stage kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   if (stage == 1) {
     p->stage1_done = true;
     p->u1_guards_valid = false;
+    p->u1_pushed = push != nullptr;
   } else {
     p->stage1_done = false;
     p->u1_guards_valid = false;
+    p->u1_pushed = false;
     p->guards_valid = false;
+    p->guards_pushed = push != nullptr;
     p->records_valid = true;
   }
   return ORCHA_OK;

@@ -154,8 +154,11 @@ int32_t orcha_packet_unpack_device(const orcha_packet* packet, double* d_interio
  * block (faces, edges and corners, depth ng) gets the value of the global
  * axis-ordered ghost fill (x, then y over x-guards, then z over x,y-guards):
  * a neighbour's interior cell or the physical boundary image.  Pure copies,
- * bitwise.  The first call with a given packet set builds and caches the
- * neighbour tables (host + one device upload); later calls only launch.
+ * bitwise.  (In the default GATHER fill mode -- orcha_set_fill_mode -- a
+ * single packet with all sources resident gets only its x-guards written here;
+ * the advance composes the rest while staging.)  The first call with a given
+ * packet set builds and caches the neighbour tables (host + one device
+ * upload); later calls only launch.
  * Errors: ORCHA_E_RANGE (a needed block is not resident and comm is NULL),
  * ORCHA_E_ARG, ORCHA_E_CUDA, ORCHA_E_NCCL. */
 int32_t orcha_fill_guardcells(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
@@ -239,6 +242,17 @@ int64_t orcha_launch_count(void);
  * build.  Errors: ORCHA_E_ARG for another value. */
 int32_t orcha_set_kernel_variant(int32_t variant);
 int32_t orcha_get_kernel_variant(void);
+
+/* Fill mode.  1 = GATHER (default): for a single packet whose guard sources
+ * are all resident, with the fused kernels, orcha_fill_guardcells writes only
+ * the x-guards, and stage 1 of the next advance / orcha_hydro_stage(.., 1, ..)
+ * stages each y/z guard row straight from the block that owns it (that
+ * block's padded row, x-guards included): the same axis-ordered ghost-fill
+ * values, composed while loading (P:L668-669's refresh, done by the consumer).
+ * 0 = FULL: the fill materialises every guard cell (the packet's guard cells
+ * then hold the documented values; multi-packet sets and remote sources always
+ * use FULL).  ORCHA_FILL_MODE=0 selects FULL at load.  Errors: ORCHA_E_ARG. */
+int32_t orcha_set_fill_mode(int32_t mode);
 
 /* Guard push (default OFF -- measured slower than the gather fill on B200,
  * DESIGN.md 6; ORCHA_PUSH=1 in the environment turns it on at load): the

@@ -26,7 +26,7 @@ EXPORTS = [
     "orcha_build_is_parity", "orcha_launch_count", "orcha_last_error", "orcha_comm_unique_id",
     "orcha_comm_create", "orcha_comm_destroy", "orcha_set_kernel_variant", "orcha_get_kernel_variant",
     "orcha_comm_create_local", "orcha_comm_push", "orcha_comm_plan", "orcha_hydro_stage",
-    "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push",
+    "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push", "orcha_set_fill_mode",
 ]
 
 
@@ -99,6 +99,7 @@ _SIGS = {
     "orcha_comm_push": (_i32, [_vp, _P(_vp), _i32, _i32, _vp]),
     "orcha_hydro_stage": (_i32, [_vp, _i32, _dbl, _vp]),
     "orcha_set_guard_push": (_i32, [_i32]),
+    "orcha_set_fill_mode": (_i32, [_i32]),
     "orcha_hydro_stage_devdt": (_i32, [_vp, _i32, _vp, _vp]),
     "orcha_fill_guardcells_stage": (_i32, [_P(_vp), _i32, _vp, _i32, _vp]),
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),

@@ -60,6 +60,43 @@ __global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict
   }
 }
 
+// x-guards only (gather mode: the fused stage 1 stages its y/z guard rows from
+// the owning blocks, whose x-guards this fills).  One thread per x-guard cell.
+__global__ void __launch_bounds__(256) fill_x_kernel(DevGrid G, double* __restrict__ state, long long total,
+                                                     const NbrEntry* __restrict__ table) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int g = G.gd[0], n0 = G.nb[0];
+  int q = (int)(t % (2 * g));
+  long long r = t / (2 * g);
+  int j = (int)(r % G.nb[1]);
+  r /= G.nb[1];
+  int k = (int)(r % G.nb[2]);
+  long long slot = r / G.nb[2];
+  const int side = q >= g;
+  const int l = side ? n0 + (q - g) : q - g;
+  const NbrEntry e = table[slot * 27 + (side ? 14 : 12)];
+  if (e.src == nullptr) return;  // remote: exchanged
+  const int m = e.mode & 3;
+  const int sx = (m == kShift) ? l - (side ? n0 : -n0) : (m == kClamp) ? (side ? n0 - 1 : 0)
+                                                                      : (side ? 2 * n0 - 1 - l : -1 - l);
+  const long long so = cell_off(G, sx, j, k);
+  double* dst = state + slot * kNVar * G.cube + cell_off(G, l, j, k);
+#pragma unroll
+  for (int v = 0; v < kNVar; v++) {
+    double x = e.src[v * G.cube + so];
+    if ((e.flip >> v) & 1) x = -x;
+    dst[v * G.cube] = x;
+  }
+}
+
+cudaError_t launch_fill_x(const DevGrid& G, double* state, int nslots, const NbrEntry* table, cudaStream_t s) {
+  long long total = (long long)nslots * G.nb[2] * G.nb[1] * 2 * G.gd[0];
+  fill_x_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(G, state, total, table);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
                         cudaStream_t s, bool faces_only) {
   long long total = (long long)nslots * G.P[0] * G.P[1] * G.P[2];

@@ -96,13 +96,22 @@ struct Geo {
   static constexpr int NW = (NB >= 16) ? (NSLOT + 1) / 2 : (W * W + 31) / 32;
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64;
+  // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
+  static constexpr size_t SMEM =
+      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64 + ((NS * IR + 15) / 16) * 16;
   // CTAs per SM we aim for: shared memory bound (227 KB per SM), at most 4
   static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
   static constexpr int MINB = MINB_S < 1 ? 1 : (MINB_S > 4 ? 4 : MINB_S);
   static_assert(NT >= FZ, "one update cell per thread");
   static_assert((BAND * 8) % 16 == 0, "bulk copies need 16-byte multiples");
 };
+
+// Interior coordinate whose value the guard coordinate c (side o = -1/0/+1
+// of an axis of NB cells) takes under neighbour-table mode m.
+template <int NB>
+__device__ __forceinline__ int guard_image(int c, int o, int m) {
+  return o == 0 ? c : m == kShift ? c - o * NB : m == kClamp ? (o < 0 ? 0 : NB - 1) : (o < 0 ? -1 - c : 2 * NB - 1 - c);
+}
 
 // U1 scratch of the fused path: per (slot, var) an (n+4)^3 cube (origin -2),
 // 256-byte aligned.
@@ -115,7 +124,8 @@ template <int NB, int STAGE, int SPLIT, int MODE, bool PUSH>
 __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
-                       DtRecord* __restrict__ rec, DevStatus* st, const PushEntry* __restrict__ push) {
+                       DtRecord* __restrict__ rec, DevStatus* st, const PushEntry* __restrict__ push,
+                       const NbrEntry* __restrict__ nbr) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
   constexpr int NT = Gm::NT, H = Gm::H, ORG = Gm::ORG;
@@ -130,6 +140,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   double* Fy = Fx + 5 * Gm::FX;                          // [5][H+1][W]
   double* Fz = Fy + 5 * Gm::FY;                          // [2][5][H][W]
   uint64_t* bar = reinterpret_cast<uint64_t*>(Fz + 2 * 5 * Gm::FZ);
+  unsigned char* flipm = reinterpret_cast<unsigned char*>(bar + 8);  // [NS][IR]
 
   const int tid = threadIdx.x;
   const long long slot = blockIdx.x / Gm::NSPLIT;
@@ -148,18 +159,60 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   __syncthreads();
 
   // input plane p (0-based, z = K0 - 2 + p): padded rows [jj0, jj0 + IR) -> ring slot p % NS.
-  // Called by one thread after a CTA barrier that follows every generic
-  // access to the slot; the proxy fence orders those before the async copy.
+  // Called by warp 0 (all lanes) after a CTA barrier that follows every
+  // generic access to the slot; the proxy fence of each issuing lane orders
+  // those before its async copies.
   auto issue = [&](int p) {
     if (p < Gm::NPLANES) {
-      int s = p % NS;
-      fence_proxy_async();
-      mbar_expect_tx(&bar[s], 5u * BAND * 8u);
+      const int s = p % NS, lane = tid & 31;
+      if (STAGE == 1 && nbr != nullptr) {
+        // Gather mode: only the x-guards were filled.  Each staged row
+        // (padded plane pp, padded row pr) is the (y, z) image of a row of
+        // the block that owns it -- the neighbour table's (0, oy, oz) entry --
+        // whose x-guards are filled: the axis-ordered ghost fill composed on
+        // the fly (x, then y over x-guards, then z over x,y-guards).  Lane r
+        // resolves row r; rows whose sources are consecutive form one copy,
+        // issued by the lane that starts the run.
+        const int pp = p + ORG, z = pp - INO;
+        const int oz = z < 0 ? -1 : (z >= NB ? 1 : 0);
+        const double* rp = nullptr;
+        int fl = 0;
+        if (lane < Gm::IR) {
+          const int pr = jj0 + ORG + lane, y = pr - INO;
+          const int oy = y < 0 ? -1 : (y >= NB ? 1 : 0);
+          const NbrEntry e = nbr[slot * 27 + (oz + 1) * 9 + (oy + 1) * 3 + 1];
+          if (e.src == nullptr) {  // remote source: its rows were exchanged into our own guards
+            rp = in + (long long)pp * Gm::PLANE + (long long)pr * IPX;
+          } else {
+            const int ys = guard_image<NB>(y, oy, (e.mode >> 2) & 3), zs = guard_image<NB>(z, oz, (e.mode >> 4) & 3);
+            rp = e.src + (long long)(zs + INO) * Gm::PLANE + (long long)(ys + INO) * IPX;
+            fl = e.flip & 0xC;  // mirrored y -> negate rho*v (bit 2), z -> rho*w (bit 3)
+          }
+          flipm[s * Gm::IR + lane] = (unsigned char)fl;
+        }
+        const double* prev = (const double*)__shfl_up_sync(0xffffffffu, (unsigned long long)rp, 1);
+        const int pfl = __shfl_up_sync(0xffffffffu, fl, 1);
+        const bool start = lane < Gm::IR && (lane == 0 || rp != prev + IPX || fl != pfl);
+        const unsigned starts = __ballot_sync(0xffffffffu, start);
+        if (lane == 0) mbar_expect_tx(&bar[s], 5u * BAND * 8u);
+        __syncwarp();
+        if (start) {
+          const unsigned later = starts & ~((2u << lane) - 1u);
+          const int run = (later ? __ffs(later) - 1 : Gm::IR) - lane;
+          fence_proxy_async();
 #pragma unroll
-      for (int v = 0; v < 5; v++)
-        bulk_load(ring + (s * 5 + v) * BAND,
-                  in + v * in_cube + (long long)(p + ORG) * Gm::PLANE + (long long)(jj0 + ORG) * IPX, BAND * 8u,
-                  &bar[s]);
+          for (int v = 0; v < 5; v++)
+            bulk_load(ring + (s * 5 + v) * BAND + lane * IPX, rp + v * in_cube, (uint32_t)(run * IPX * 8), &bar[s]);
+        }
+      } else if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar[s], 5u * BAND * 8u);
+#pragma unroll
+        for (int v = 0; v < 5; v++)
+          bulk_load(ring + (s * 5 + v) * BAND,
+                    in + v * in_cube + (long long)(p + ORG) * Gm::PLANE + (long long)(jj0 + ORG) * IPX, BAND * 8u,
+                    &bar[s]);
+      }
     }
   };
   auto wait_plane = [&](int p) { mbar_wait(&bar[p % NS], (p / NS) & 1); };
@@ -169,8 +222,14 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     unsigned long long hits = 0;
     for (int c = tid; c < BAND; c += NT) {
       bool fl;
-      Prim q = eos(Q[c], Q[BAND + c], Q[2 * BAND + c], Q[3 * BAND + c], Q[4 * BAND + c], G, &fl);
       int r = c / IPX;
+      double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
+      if (STAGE == 1 && nbr != nullptr) {  // gather mode: mirrored guard rows negate rho*v / rho*w
+        const unsigned fm = flipm[(p % NS) * Gm::IR + r];
+        if (fm & 4) my = -my;
+        if (fm & 8) mz = -mz;
+      }
+      Prim q = eos(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl);
       int x = c - r * IPX - INO, y = jj0 + ORG + r - INO;
       // own (non-overlapping) rows of the band only, so each cell counts once
       bool mine = r >= 2 && r < 2 + H;
@@ -260,8 +319,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   }
 
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
-  if (tid == 0)
+  if (tid < 32)
     for (int p = 0; p < NS; p++) issue(p);
+  if (STAGE == 1 && nbr != nullptr) __syncthreads();  // the sign-flip masks thread 0 just wrote
   for (int p = 0; p < 5; p++) {
     wait_plane(p);
     convert(p);
@@ -269,7 +329,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   __syncthreads();
   for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
   __syncthreads();
-  if (tid == 0) issue(5);  // into the slot of plane 0
+  if (tid < 32) issue(5);  // into the slot of plane 0
 
   double s_rec = -DBL_MAX;
   long long g_rec = LLONG_MAX;
@@ -283,8 +343,26 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     const long long so = cell_off(G, ci, cj, k);
     double un[5], v1[5];
     if (upd) {
+      const double* ub = state + slot * 5 * cube;
+      long long uo = so;
+      int ufl = 0;
+      if (STAGE == 1 && MODE == 0 && nbr != nullptr) {
+        // gather mode: the box's y/z guard-ring cells were not filled; U^n of
+        // such a cell is its image in the owning block (x-guards are filled)
+        const int oy = cj < 0 ? -1 : (cj >= NB ? 1 : 0), oz = k < 0 ? -1 : (k >= NB ? 1 : 0);
+        if (oy != 0 || oz != 0) {
+          const NbrEntry e = nbr[slot * 27 + (oz + 1) * 9 + (oy + 1) * 3 + 1];
+          if (e.src != nullptr) {
+            ub = e.src;
+            uo = cell_off(G, ci, guard_image<NB>(cj, oy, (e.mode >> 2) & 3), guard_image<NB>(k, oz, (e.mode >> 4) & 3));
+            ufl = e.flip & 0xC;
+          }
+        }
+      }
 #pragma unroll
-      for (int v = 0; v < 5; v++) un[v] = __ldg(state + slot * 5 * cube + v * cube + so);
+      for (int v = 0; v < 5; v++) un[v] = __ldg(ub + v * cube + uo);
+      if (ufl & 4) un[2] = -un[2];
+      if (ufl & 8) un[3] = -un[3];
       if (STAGE == 2) {
         const long long uo = u1_off(ci, cj, k);
 #pragma unroll
@@ -302,7 +380,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     __syncthreads();
     // phase 2: stage plane it+6 into the slot of plane it+1 (read for the
     // last time in phase 1), convert plane it+5, update the band's cells
-    if (tid == 0) issue(it + 6);
+    if (tid < 32) issue(it + 6);
     if (it + 5 < Gm::NPLANES) {
       wait_plane(it + 5);
       convert(it + 5);
@@ -355,7 +433,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 template <int NB, int STAGE, int SPLIT, int MODE>
 static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                          const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s,
-                         const PushEntry* push = nullptr) {
+                         const PushEntry* push = nullptr, const NbrEntry* nbr = nullptr) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   static bool attr = false;
   if (!attr) {
@@ -369,10 +447,10 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
   // kernels carry none of its register pressure
   if (push)
     stage_fused_kernel<NB, STAGE, SPLIT, MODE, true><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, push);
+        G, state, u1, slots, d_dt, h_dt, records, st, push, nbr);
   else
     stage_fused_kernel<NB, STAGE, SPLIT, MODE, false><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, nullptr);
+        G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nbr);
   count_launch();
 }
 
@@ -388,22 +466,22 @@ static int split_env(const char* name, int dflt) {
 template <int NB>
 static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
-                             cudaStream_t s, const PushEntry* push) {
+                             cudaStream_t s, const PushEntry* push, const NbrEntry* nbr) {
   int s2 = 1;
   if constexpr (NB == 16) {
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
     static const int s2v = split_env("ORCHA_SPLIT2", 2);
     s2 = s2v;
-    if (s1 == 4) launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
-    else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    if (s1 == 4) launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
   } else if constexpr (NB == 32) {
-    launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     s2 = 4;
   } else {
-    launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s);
+    launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
   }
   *nrecords = (long long)nslots * s2;
@@ -420,44 +498,50 @@ cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double*
 // The fused path covers 3D blocks of 8^3, 16^3 and 32^3 with ng = 4 (the
 // paper's "typical block in AMR is 16^3"; BASELINE configs[4]
 // sweeps 8^3 / 16^3 / 32^3); other shapes use the reference kernels (same
-// results, no guard push).
+// results, no guard push, no gather mode).
 bool fused_supported(const DevGrid& G) {
   return G.ndim == 3 && G.ng == 4 && G.nb[0] == G.nb[1] && G.nb[1] == G.nb[2] &&
          (G.nb[0] == 16 || G.nb[0] == 8 || G.nb[0] == 32);
 }
 
 // `push` (optional): the per-slot push tables of the packet's state; when
-// given, stage 2 also scatters U^{n+1} into the guards of the resident blocks
-// (push.cuh), which makes the next gather fill unnecessary.
+// given, stage 2 also scatters U^{n+1} into the guards of same-packet blocks
+// (push.cuh).  `nbr` (optional, gather mode): the per-slot neighbour tables;
+// stage 1 then stages its y/z guard rows straight from the owning blocks and
+// needs only the x-guards filled.
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
-                                 DevStatus* st, cudaStream_t s, const PushEntry* push) {
+                                 DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr) {
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  if (G.nb[0] == 16) return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push);
-  if (G.nb[0] == 32) return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push);
-  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push);
+  if (G.nb[0] == 16)
+    return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr);
+  if (G.nb[0] == 32)
+    return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr);
+  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr);
 }
 
 // One stage of the per-stage variant (F1): stage 1 -> U1 (padded, interior
 // only), stage 2 -> U^{n+1} in place + dt records.  `push` (optional): the
 // push tables of the buffer this stage writes (stage 1: the stage-1 buffers,
-// stage 2: the states).
+// stage 2: the states); `nbr` (optional, stage 1, gather mode) as above.
 cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
-                               long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push) {
+                               long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
+                               const NbrEntry* nbr) {
   if (!fused_supported(G))
     return launch_stage_ref(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
+  const NbrEntry* n1 = (stage == 1) ? nbr : nullptr;
   if (G.nb[0] == 16) {
-    if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, n1);
     else launch_stage<16, 2, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     if (stage == 2) *nrecords = (long long)nslots * 2;
   } else if (G.nb[0] == 32) {
-    if (stage == 1) launch_stage<32, 1, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    if (stage == 1) launch_stage<32, 1, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, n1);
     else launch_stage<32, 2, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     if (stage == 2) *nrecords = (long long)nslots * 4;
   } else {
-    if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, n1);
     else launch_stage<8, 2, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
     if (stage == 2) *nrecords = (long long)nslots;
   }

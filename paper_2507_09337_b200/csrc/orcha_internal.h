@@ -107,6 +107,10 @@ struct orcha_packet {
   const FillPlan* push_plan;          // the plan those tables belong to
   bool guards_pushed;          // the last state update scattered itself into the guards (push_plan)
   bool u1_pushed;              // same for the stage-1 buffer
+  // gather mode: the last state fill wrote only the x-guards; stage 1 stages
+  // the y/z guard rows from the owning blocks through d_nbr
+  bool guards_xonly;
+  const orcha::NbrEntry* d_nbr;
 };
 
 namespace orcha {
@@ -124,6 +128,7 @@ long long records_capacity(const DevGrid& G, long long nslots);
 // kernel launchers (kernels_*.cu); all return cudaGetLastError()
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
                         cudaStream_t s, bool faces_only = false);
+cudaError_t launch_fill_x(const DevGrid& G, double* state, int nslots, const NbrEntry* table, cudaStream_t s);
 cudaError_t launch_pack(const DevGrid& G, double* state, const double* staged, int nslots,
                         bool to_state, cudaStream_t s);
 cudaError_t launch_status_reset(DevStatus* st, cudaStream_t s);

@@ -56,15 +56,34 @@ cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int 
                                DevStatus* st, cudaStream_t s);
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
-                                 DevStatus* st, cudaStream_t s, const PushEntry* push);
+                                 DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr);
 cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                              const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                              long long* nrecords, DevStatus* st, cudaStream_t s);
 cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
-                               long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push);
+                               long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
+                               const NbrEntry* nbr);
 bool fused_supported(const DevGrid& G);
 }  // namespace orcha
+
+// Fill mode: 1 = gather (default): when every guard source of the packet set
+// is resident and the fused kernels run, the state fill writes only the
+// x-guards and stage 1 stages its y/z guard rows straight from the owning
+// blocks (kernels_fused.cu); 0 = full: the fill materialises every guard.
+static int g_fill_mode = -1;
+static int fill_mode() {
+  if (g_fill_mode < 0) {
+    const char* e = getenv("ORCHA_FILL_MODE");
+    g_fill_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_fill_mode;
+}
+extern "C" int32_t orcha_set_fill_mode(int32_t mode) {
+  if (mode != 0 && mode != 1) return fail(ORCHA_E_ARG, "fill mode must be 0 (full) or 1 (gather)");
+  g_fill_mode = mode;
+  return ORCHA_OK;
+}
 
 // Guard push on/off.  Default OFF: measured on cfg4 the per-cell scatter in
 // the stage-2 epilogue costs more (+1.0 ms) than the gather fill it removes
@@ -244,6 +263,8 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
   p->d_push = p->d_push_u1 = nullptr;
   p->push_plan = nullptr;
   p->guards_pushed = p->u1_pushed = false;
+  p->guards_xonly = false;
+  p->d_nbr = nullptr;
   std::vector<SlotInfo> si(n);
   const DevGrid& G = g->dev;
   for (int s = 0; s < n; s++) {
@@ -589,12 +610,24 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   bool all_pushed = push_enabled();
   for (int q = 0; q < npk; q++)
     all_pushed &= pk[q]->push_plan == f && (buffer ? pk[q]->u1_pushed : pk[q]->guards_pushed);
+  // gather mode (state only, fused kernels, ONE packet with every source
+  // resident): x-guards only.  With several packets the advances run one after
+  // another and a later packet's stage 1 would read a neighbour packet's
+  // already-advanced interior, so multi-packet sets keep the full fill.
+  const DevGrid& G0 = pk[0]->grid->dev;
+  const bool xonly = buffer == 0 && npk == 1 && !all_pushed && fill_mode() == 1 && !f->has_remote &&
+                     kernel_variant() == 1 && fused_supported(G0);
   for (int q = 0; q < npk; q++) {
     double* dst = buffer ? pk[q]->scratch : pk[q]->state;
-    const NbrEntry* tab = all_pushed ? (buffer ? f->d_cross_u1[q] : f->d_cross[q])   // cross-packet only
-                                     : (buffer ? f->d_tables_u1[q] : f->d_tables[q]);
-    if (!tab) continue;  // pushed, and no source in another packet
-    cudaError_t e = launch_fill(pk[q]->grid->dev, dst, pk[q]->nslots, tab, s, faces_only);
+    cudaError_t e;
+    if (xonly) {
+      e = launch_fill_x(G0, dst, pk[q]->nslots, f->d_tables[q], s);
+    } else {
+      const NbrEntry* tab = all_pushed ? (buffer ? f->d_cross_u1[q] : f->d_cross[q])   // cross-packet only
+                                       : (buffer ? f->d_tables_u1[q] : f->d_tables[q]);
+      if (!tab) continue;  // pushed, and no source in another packet
+      e = launch_fill(pk[q]->grid->dev, dst, pk[q]->nslots, tab, s, faces_only);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   }
   for (int q = 0; q < npk; q++) {
@@ -605,8 +638,11 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
       pk[q]->u1_guards_valid = true;
     } else {
       pk[q]->guards_valid = true;
-      // a push writes every same-packet guard; cross-packet ones are full unless faces-only
-      pk[q]->guards_full = !faces_only || (all_pushed && f->d_cross[q] == nullptr);
+      pk[q]->guards_xonly = xonly;
+      pk[q]->d_nbr = f->d_tables[q];
+      // a push writes every same-packet guard; cross-packet ones are full unless faces-only;
+      // in gather mode stage 1 composes the y/z guards itself
+      pk[q]->guards_full = xonly || !faces_only || (all_pushed && f->d_cross[q] == nullptr);
     }
   }
   return ORCHA_OK;
@@ -678,13 +714,15 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   const DevGrid& G = p->grid->dev;
   cudaError_t e;
   const bool fused = kernel_variant() == 1;
+  if (p->guards_xonly && !fused)
+    return fail(ORCHA_E_STATE, "the gather-mode fill was done for the fused kernels; refill after changing the variant");
   const PushEntry* push = (fused && push_enabled() && fused_supported(G) && p->push_plan) ? p->d_push : nullptr;
   if (!fused)
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
   else
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                             &p->nrecords, p->status, s, push);
+                             &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "advance kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   p->guards_valid = false;
@@ -716,6 +754,8 @@ static int32_t stage_impl(orcha_packet* p, int32_t stage, const double* d_dt, do
   const DevGrid& G = p->grid->dev;
   cudaError_t e;
   const bool fused = kernel_variant() == 1;
+  if (stage == 1 && p->guards_xonly && !fused)
+    return fail(ORCHA_E_STATE, "the gather-mode fill was done for the fused kernels; refill after changing the variant");
   const PushEntry* push = nullptr;
   if (fused && push_enabled() && fused_supported(G) && p->push_plan) push = (stage == 1) ? p->d_push_u1 : p->d_push;
   if (!fused)
@@ -723,7 +763,7 @@ static int32_t stage_impl(orcha_packet* p, int32_t stage, const double* d_dt, do
                          &p->nrecords, p->status, s);
   else
     e = launch_stage_fused(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                           &p->nrecords, p->status, s, push);
+                           &p->nrecords, p->status, s, push, (stage == 1 && p->guards_xonly) ? p->d_nbr : nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "stage kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   if (stage == 1) {

@@ -51,8 +51,12 @@ def test_guard_fill_equals_global_ghost_fill(bcode, ndim, nb, nblk, npk):
     og = H.oracle_grid(g)
     U0 = inp.random_field(g.N[:ndim], seed=9)
     pk = H.gpu_setup(g, U0, npackets=npk, shuffle=True)
-    from paper_2507_09337_b200 import hydro
-    hydro.orcha_fill_guardcells(pk)
+    from paper_2507_09337_b200 import abi, hydro
+    abi.call(g.lib, "orcha_set_fill_mode", 0)   # FULL: materialise every guard
+    try:
+        hydro.orcha_fill_guardcells(pk)
+    finally:
+        abi.call(g.lib, "orcha_set_fill_mode", 1)
     Ug = oracle.padded(og, U0)
     oracle.fill_ghosts(og, Ug)
     ng = 4

@@ -120,7 +120,9 @@ __host__ __device__ constexpr long long u1_cube() {
   return ((long long)(NB + 4) * (NB + 4) * (NB + 4) * 8 + 255) / 256 * 256 / 8;
 }
 
-template <int NB, int STAGE, int SPLIT, int MODE, bool PUSH>
+// PUSH: 0 none, 1 scatter the new state into every same-packet guard
+// (push_cell), 2 into the x-guards only (push_cell_x, gather mode).
+template <int NB, int STAGE, int SPLIT, int MODE, int PUSH>
 __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
@@ -152,6 +154,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const long long in_cube = (STAGE == 1) ? cube : U1C;
   const SlotInfo si = slots[slot];
 
+  __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
+  if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
@@ -412,7 +416,23 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         double* dst = state + slot * 5 * cube + so;
 #pragma unroll
         for (int v = 0; v < 5; v++) dst[v * cube] = nw[v];
-        if (PUSH) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
+        if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
+        if (PUSH == 2) {  // x-guards only (the x-axis part of push_cell; both entries cached in shared memory)
+          const int side = ci >= NB - 4 ? 1 : (ci < 4 ? 0 : -1);
+          if (side >= 0 && sxp[side].dst != nullptr) {
+            const PushEntry e = sxp[side];
+            const int m = e.mode & 3;
+            int t0, cnt = 1;
+            if (m == kShift) t0 = side ? ci - NB : ci + NB;
+            else if (m == kMirror) t0 = side ? 2 * NB - 1 - ci : -1 - ci;
+            else { cnt = (side ? ci == NB - 1 : ci == 0) ? 4 : 0; t0 = side ? NB : -4; }
+            for (int xx = 0; xx < cnt; xx++) {
+              double* q = e.dst + cell_off(G, t0 + xx, cj, k);
+#pragma unroll
+              for (int v = 0; v < 5; v++) q[v * cube] = ((e.flip >> v) & 1) ? -nw[v] : nw[v];
+            }
+          }
+        }
         bool f2;
         Prim q = eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
         double s = signal_speed<3>(q, G);
@@ -433,23 +453,29 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 template <int NB, int STAGE, int SPLIT, int MODE>
 static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                          const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s,
-                         const PushEntry* push = nullptr, const NbrEntry* nbr = nullptr) {
+                         const PushEntry* push = nullptr, const NbrEntry* nbr = nullptr, int pushkind = 1) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Gm::SMEM);
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Gm::SMEM);
+    if (STAGE == 2 && MODE == 0)
+      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
     attr = true;
   }
-  // the guard-push epilogue is a separate instantiation so the default
-  // kernels carry none of its register pressure
-  if (push)
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, true><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
+  // the guard-push epilogues are separate instantiations so the default
+  // kernels carry none of their register pressure
+  if (push && pushkind == 2 && STAGE == 2 && MODE == 0)
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, (STAGE == 2 && MODE == 0) ? 2 : 1>
+        <<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, d_dt, h_dt, records, st, push, nbr);
+  else if (push)
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
         G, state, u1, slots, d_dt, h_dt, records, st, push, nbr);
   else
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, false><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
         G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nbr);
   count_launch();
 }
@@ -466,7 +492,7 @@ static int split_env(const char* name, int dflt) {
 template <int NB>
 static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
-                             cudaStream_t s, const PushEntry* push, const NbrEntry* nbr) {
+                             cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk) {
   int s2 = 1;
   if constexpr (NB == 16) {
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
@@ -474,15 +500,15 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
     s2 = s2v;
     if (s1 == 4) launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
-    else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
   } else if constexpr (NB == 32) {
     launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
     s2 = 4;
   } else {
     launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
   }
   *nrecords = (long long)nslots * s2;
   return cudaGetLastError();
@@ -511,14 +537,16 @@ bool fused_supported(const DevGrid& G) {
 // needs only the x-guards filled.
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
-                                 DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr) {
+                                 DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr,
+                                 bool push_x_only) {
+  const int pk = push_x_only ? 2 : 1;
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   if (G.nb[0] == 16)
-    return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr);
+    return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk);
   if (G.nb[0] == 32)
-    return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr);
-  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr);
+    return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk);
+  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk);
 }
 
 // One stage of the per-stage variant (F1): stage 1 -> U1 (padded, interior

@@ -107,6 +107,7 @@ struct orcha_packet {
   const FillPlan* push_plan;          // the plan those tables belong to
   bool guards_pushed;          // the last state update scattered itself into the guards (push_plan)
   bool u1_pushed;              // same for the stage-1 buffer
+  bool xguards_pushed;         // the last advance scattered U^{n+1} into the x-guards only (gather mode)
   // gather mode: the last state fill wrote only the x-guards; stage 1 stages
   // the y/z guard rows from the owning blocks through d_nbr
   bool guards_xonly;

@@ -56,7 +56,8 @@ cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int 
                                DevStatus* st, cudaStream_t s);
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
-                                 DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr);
+                                 DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr,
+                                 bool push_x_only);
 cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                              const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                              long long* nrecords, DevStatus* st, cudaStream_t s);
@@ -263,6 +264,7 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
   p->d_push = p->d_push_u1 = nullptr;
   p->push_plan = nullptr;
   p->guards_pushed = p->u1_pushed = false;
+  p->xguards_pushed = false;
   p->guards_xonly = false;
   p->d_nbr = nullptr;
   std::vector<SlotInfo> si(n);
@@ -324,6 +326,7 @@ static int32_t pack_impl(orcha_packet* p, const double* src, cudaMemcpyKind kind
   p->stage1_done = false;       // the staging area overwrote the stage-1 buffer
   p->u1_guards_valid = false;
   p->guards_pushed = p->u1_pushed = false;  // new interior, not scattered into any guards
+  p->xguards_pushed = false;
   return ORCHA_OK;
 }
 
@@ -621,6 +624,8 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
     double* dst = buffer ? pk[q]->scratch : pk[q]->state;
     cudaError_t e;
     if (xonly) {
+      // the last advance scattered U^{n+1} into the x-guards with this plan: nothing to do
+      if (pk[q]->xguards_pushed && pk[q]->push_plan == f) continue;
       e = launch_fill_x(G0, dst, pk[q]->nslots, f->d_tables[q], s);
     } else {
       const NbrEntry* tab = all_pushed ? (buffer ? f->d_cross_u1[q] : f->d_cross[q])   // cross-packet only
@@ -717,16 +722,21 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   if (p->guards_xonly && !fused)
     return fail(ORCHA_E_STATE, "the gather-mode fill was done for the fused kernels; refill after changing the variant");
   const PushEntry* push = (fused && push_enabled() && fused_supported(G) && p->push_plan) ? p->d_push : nullptr;
+  // gather mode: stage 2 scatters U^{n+1} into the x-guards (all the next
+  // gather-mode fill would write), so that fill launches nothing
+  const bool xpush = fused && !push && p->guards_xonly && p->push_plan != nullptr;
+  if (xpush) push = p->d_push;
   if (!fused)
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
   else
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                             &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr);
+                             &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr, xpush);
   if (e != cudaSuccess) return cuda_fail(e, "advance kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   p->guards_valid = false;
-  p->guards_pushed = push != nullptr;
+  p->guards_pushed = push != nullptr && !xpush;
+  p->xguards_pushed = xpush;
   p->records_valid = true;
   p->stage1_done = false;
   p->u1_guards_valid = false;
@@ -776,6 +786,7 @@ static int32_t stage_impl(orcha_packet* p, int32_t stage, const double* d_dt, do
     p->u1_pushed = false;
     p->guards_valid = false;
     p->guards_pushed = push != nullptr;
+    p->xguards_pushed = false;
     p->records_valid = true;
   }
   return ORCHA_OK;

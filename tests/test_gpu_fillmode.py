@@ -72,3 +72,20 @@ def test_variant_switch_after_gather_fill_is_refused():
         hydro.orcha_hydro_advance(pk[0], 1e-5)
     finally:
         hydro.set_kernel_variant(g.lib, 1)
+
+
+def test_gather_mode_steady_state_fill_launches_nothing():
+    # after the first advance, stage 2 has scattered U^{n+1} into the x-guards
+    # (push_cell_x), so the next gather-mode fill is a no-op on the device
+    from paper_2507_09337_b200 import hydro
+    g = H.make_grid(3, (16, 16, 16), (2, 2, 2), bc=((R, O), (P, P), (O, R)))
+    _mode(g.lib, 1)
+    pk = H.gpu_setup(g, inp.random_field(g.N, seed=3))
+    hydro.orcha_fill_guardcells(pk)
+    n0 = g.lib.orcha_launch_count()
+    hydro.orcha_fill_guardcells(pk)          # refill of unchanged guards (not pushed yet): one fill_x
+    assert g.lib.orcha_launch_count() - n0 == 1
+    hydro.orcha_hydro_advance(pk[0], 1e-5)
+    n1 = g.lib.orcha_launch_count()
+    hydro.orcha_fill_guardcells(pk)
+    assert g.lib.orcha_launch_count() == n1

@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 
   __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
   if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
+  __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
+  if (STAGE == 1 && nbr != nullptr && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         if (lane < Gm::IR) {
           const int pr = jj0 + ORG + lane, y = pr - INO;
           const int oy = y < 0 ? -1 : (y >= NB ? 1 : 0);
-          const NbrEntry e = nbr[slot * 27 + (oz + 1) * 9 + (oy + 1) * 3 + 1];
+          const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
           if (e.src == nullptr) {  // remote source: its rows were exchanged into our own guards
             rp = in + (long long)pp * Gm::PLANE + (long long)pr * IPX;
           } else {
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         // such a cell is its image in the owning block (x-guards are filled)
         const int oy = cj < 0 ? -1 : (cj >= NB ? 1 : 0), oz = k < 0 ? -1 : (k >= NB ? 1 : 0);
         if (oy != 0 || oz != 0) {
-          const NbrEntry e = nbr[slot * 27 + (oz + 1) * 9 + (oy + 1) * 3 + 1];
+          const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
           if (e.src != nullptr) {
             ub = e.src;
             uo = cell_off(G, ci, guard_image<NB>(cj, oy, (e.mode >> 2) & 3), guard_image<NB>(k, oz, (e.mode >> 4) & 3));

@@ -122,7 +122,9 @@ __host__ __device__ constexpr long long u1_cube() {
 
 // PUSH: 0 none, 1 scatter the new state into every same-packet guard
 // (push_cell), 2 into the x-guards only (push_cell_x, gather mode).
-template <int NB, int STAGE, int SPLIT, int MODE, int PUSH>
+// GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a
+// separate instantiation so the plain kernels carry none of its registers.
+template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER>
 __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
   if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
   __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
-  if (STAGE == 1 && nbr != nullptr && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
+  if (STAGE == 1 && GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   auto issue = [&](int p) {
     if (p < Gm::NPLANES) {
       const int s = p % NS, lane = tid & 31;
-      if (STAGE == 1 && nbr != nullptr) {
+      if (STAGE == 1 && GATHER) {
         // Gather mode: only the x-guards were filled.  Each staged row
         // (padded plane pp, padded row pr) is the (y, z) image of a row of
         // the block that owns it -- the neighbour table's (0, oy, oz) entry --
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       bool fl;
       int r = c / IPX;
       double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
-      if (STAGE == 1 && nbr != nullptr) {  // gather mode: mirrored guard rows negate rho*v / rho*w
+      if (STAGE == 1 && GATHER) {  // gather mode: mirrored guard rows negate rho*v / rho*w
         const unsigned fm = flipm[(p % NS) * Gm::IR + r];
         if (fm & 4) my = -my;
         if (fm & 8) mz = -mz;
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
   if (tid < 32)
     for (int p = 0; p < NS; p++) issue(p);
-  if (STAGE == 1 && nbr != nullptr) __syncthreads();  // the sign-flip masks thread 0 just wrote
+  if (STAGE == 1 && GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
   for (int p = 0; p < 5; p++) {
     wait_plane(p);
     convert(p);
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       const double* ub = state + slot * 5 * cube;
       long long uo = so;
       int ufl = 0;
-      if (STAGE == 1 && MODE == 0 && nbr != nullptr) {
+      if (STAGE == 1 && MODE == 0 && GATHER) {
         // gather mode: the box's y/z guard-ring cells were not filled; U^n of
         // such a cell is its image in the owning block (x-guards are filled)
         const int oy = cj < 0 ? -1 : (cj >= NB ? 1 : 0), oz = k < 0 ? -1 : (k >= NB ? 1 : 0);
@@ -459,26 +461,37 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Gm::SMEM);
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Gm::SMEM);
-    if (STAGE == 2 && MODE == 0)
-      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gm::SMEM);
+    const int sm = (int)Gm::SMEM;
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if constexpr (STAGE == 1)
+      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if constexpr (STAGE == 2 && MODE == 0)
+      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     attr = true;
   }
-  // the guard-push epilogues are separate instantiations so the default
-  // kernels carry none of their register pressure
-  if (push && pushkind == 2 && STAGE == 2 && MODE == 0)
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, (STAGE == 2 && MODE == 0) ? 2 : 1>
-        <<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, d_dt, h_dt, records, st, push, nbr);
-  else if (push)
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, push, nbr);
-  else
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0><<<nslots * SPLIT, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nbr);
+  // the guard-push epilogues and the gather staging are separate
+  // instantiations so the default kernels carry none of their registers
+  const dim3 grid(nslots * SPLIT);
+  if (push && pushkind == 2) {
+    if constexpr (STAGE == 2 && MODE == 0)
+      stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false><<<grid, Gm::NT, Gm::SMEM, s>>>(
+          G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr);
+  } else if (push) {
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false><<<grid, Gm::NT, Gm::SMEM, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr);
+  } else if (nbr) {
+    if constexpr (STAGE == 1)
+      stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true><<<grid, Gm::NT, Gm::SMEM, s>>>(
+          G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nbr);
+  } else {
+    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false><<<grid, Gm::NT, Gm::SMEM, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nullptr);
+  }
   count_launch();
 }
 

@@ -616,9 +616,10 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   // gather mode (state only, fused kernels, ONE packet with every source
   // resident): x-guards only.  With several packets the advances run one after
   // another and a later packet's stage 1 would read a neighbour packet's
-  // already-advanced interior, so multi-packet sets keep the full fill.
+  // already-advanced interior, so multi-packet sets keep the full fill; so
+  // does the guard-push mode (its kernels have no gather staging).
   const DevGrid& G0 = pk[0]->grid->dev;
-  const bool xonly = buffer == 0 && npk == 1 && !all_pushed && fill_mode() == 1 && !f->has_remote &&
+  const bool xonly = buffer == 0 && npk == 1 && !push_enabled() && fill_mode() == 1 && !f->has_remote &&
                      kernel_variant() == 1 && fused_supported(G0);
   for (int q = 0; q < npk; q++) {
     double* dst = buffer ? pk[q]->scratch : pk[q]->state;

@@ -34,17 +34,20 @@ METRIC = "cell-updates/sec (fp64, 3D Sedov)"
 UNIT = "cell-updates/s"
 
 
-def algorithmic_costs(nb=16, ng=4):
+def algorithmic_costs(nb=16, ng=4, fill_mode="gather"):
     """Per cell-update algorithmic work of the telescoped 16^3 step (DESIGN.md
     section 6): bytes of the advance (read the padded block once,
-    write the interior once) and of the guard fill (read every guard's source,
-    write the guard); fp64-pipe instructions of the advance (SURVEY 8(d):
-    1498 per cell-update for the box stage-1 region, SASS-derived)."""
+    write the interior once) and of the guard fill -- full mode: read every
+    guard's source and write the guard; gather mode: stage 2 writes the
+    x-guards (the y/z guard rows are read from their owners inside the
+    advance's one read of the padded block); fp64-pipe instructions of the
+    advance (1498 per cell-update for the box stage-1 region,
+    SASS-derived)."""
     P = nb + 2 * ng
     n3 = nb ** 3
     adv_bytes = (P ** 3 + n3) * 5 * 8 / n3
     guards = P ** 3 - n3
-    fill_bytes = 2 * guards * 5 * 8 / n3
+    fill_bytes = 2 * guards * 5 * 8 / n3 if fill_mode == "full" else 2 * ng * nb * nb * 5 * 8 / n3
     return adv_bytes, fill_bytes, FP64_INSTR_PER_CU
 
 
@@ -191,6 +194,8 @@ def main():
     ap.add_argument("--method", default="telescoped", choices=["telescoped", "per-stage"],
                     help="RK2 step: the paper's telescoped step (default) or the per-stage F1 variant")
     ap.add_argument("--no-variants", action="store_true", help="skip the per-stage measurement beside the main line")
+    ap.add_argument("--fill-mode", default="gather", choices=["gather", "full"],
+                    help="guard fill: gather (x-guards only, y/z rows staged from their owners; default) or full")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -220,6 +225,7 @@ def main():
     lib = abi.load(False)
     if args.variant is not None:
         hydro.set_kernel_variant(lib, args.variant)
+    abi.call(lib, "orcha_set_fill_mode", 1 if args.fill_mode == "gather" else 0)
 
     px, py, pz = GPU_GRIDS[world]
     nblk = (BRICK_BLOCKS[0] * px, BRICK_BLOCKS[1] * py, BRICK_BLOCKS[2] * pz)
@@ -320,7 +326,10 @@ def main():
 
     # roofline of the dominant kernel (the advance): algorithmic bytes / flops
     pks = peaks()
-    adv_bytes, fill_bytes, fp_instr = algorithmic_costs()
+    # gather mode needs every neighbour resident (one GPU); with remote
+    # neighbours the library runs the full fill + exchange
+    fill_eff = args.fill_mode if world == 1 else "full"
+    adv_bytes, fill_bytes, fp_instr = algorithmic_costs(fill_mode=fill_eff)
     cu_local = BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2] * NB[0] * NB[1] * NB[2]
     hbm_achieved = adv_bytes * cu_local / (adv_ms / 1e3) / 1e9
     fp_achieved = fp_instr * cu_local / (adv_ms / 1e3) / 1e12
@@ -373,7 +382,7 @@ def main():
             "config": {"workload": "cfg4: 3D Sedov, 4096 blocks of 16^3 (+4 guards) per GPU, one packet",
                        "global_cells": list(N), "blocks_per_gpu": int(len(ids)), "gpu_grid": list(GPU_GRIDS[world]),
                        "ng": 4, "gamma": 1.4, "cfl": 0.4, "l2_flush": "not needed: 2.2 GB state per GPU >> 126 MB L2",
-                       "kernel_variant": int(lib.orcha_get_kernel_variant()),
+                       "kernel_variant": int(lib.orcha_get_kernel_variant()), "fill_mode": fill_eff,
                        "global_batch": None, "seq_len": None, "parallelism": f"blocks over {world} GPU(s)"},
             "roofline": primary, "roofline_other": other,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],

@@ -249,9 +249,13 @@ int32_t orcha_get_kernel_variant(void);
  * stages each y/z guard row straight from the block that owns it (that
  * block's padded row, x-guards included): the same axis-ordered ghost-fill
  * values, composed while loading (P:L668-669's refresh, done by the consumer).
- * 0 = FULL: the fill materialises every guard cell (the packet's guard cells
- * then hold the documented values; multi-packet sets and remote sources always
- * use FULL).  ORCHA_FILL_MODE=0 selects FULL at load.  Errors: ORCHA_E_ARG. */
+ * Stage 2 of orcha_hydro_advance then writes U^{n+1} into the x-guards too, so
+ * the next fill of the same packet launches nothing.  In this mode the y/z
+ * guard cells of the state are NOT materialised (read them only after a FULL
+ * fill).  0 = FULL: the fill materialises every guard cell (the packet's guard
+ * cells then hold the documented values; multi-packet sets, remote sources and
+ * the guard-push mode always use FULL).  ORCHA_FILL_MODE=0 selects FULL at
+ * load.  Errors: ORCHA_E_ARG. */
 int32_t orcha_set_fill_mode(int32_t mode);
 
 /* Guard push (default OFF -- measured slower than the gather fill on B200,

@@ -326,9 +326,9 @@ def main():
 
     # roofline of the dominant kernel (the advance): algorithmic bytes / flops
     pks = peaks()
-    # gather mode needs every neighbour resident (one GPU); with remote
-    # neighbours the library runs the full fill + exchange
-    fill_eff = args.fill_mode if world == 1 else "full"
+    # (N > 1: the remote guards are exchanged into each rank's packet first;
+    # the local part of the fill follows the mode)
+    fill_eff = args.fill_mode
     adv_bytes, fill_bytes, fp_instr = algorithmic_costs(fill_mode=fill_eff)
     cu_local = BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2] * NB[0] * NB[1] * NB[2]
     hbm_achieved = adv_bytes * cu_local / (adv_ms / 1e3) / 1e9

@@ -18,6 +18,10 @@ namespace orcha {
 __global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict__ state,
                                                    long long total, const NbrEntry* __restrict__ table,
                                                    int faces_only, int depth) {
+  // faces_only: 0 every guard, 1 face guards to `depth`, 2 the gather-mode
+  // complement: x-guard cells of the y/z-guard rows whose row source is
+  // remote (the exchange wrote the row's interior part into our guards; the
+  // parts sourced from resident blocks are written here)
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   long long cells = (long long)G.P[0] * G.P[1] * G.P[2];
@@ -31,7 +35,10 @@ __global__ void __launch_bounds__(256) fill_kernel(DevGrid G, double* __restrict
 #pragma unroll
   for (int d = 0; d < 3; d++) o[d] = (l[d] < 0) ? -1 : (l[d] >= G.nb[d]) ? 1 : 0;
   if (o[0] == 0 && o[1] == 0 && o[2] == 0) return;
-  if (faces_only) {
+  if (faces_only == 2) {
+    if (o[0] == 0 || (o[1] == 0 && o[2] == 0)) return;
+    if (table[slot * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + 1].src != nullptr) return;  // row gathered by stage 1
+  } else if (faces_only) {
     int outside = (o[0] != 0) + (o[1] != 0) + (o[2] != 0);
     bool deep = false;
 #pragma unroll
@@ -98,10 +105,10 @@ cudaError_t launch_fill_x(const DevGrid& G, double* state, int nslots, const Nbr
 }
 
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
-                        cudaStream_t s, bool faces_only) {
+                        cudaStream_t s, int faces_only) {
   long long total = (long long)nslots * G.P[0] * G.P[1] * G.P[2];
   long long blocks = (total + 255) / 256;
-  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(G, state, total, table, faces_only ? 1 : 0, 2);
+  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(G, state, total, table, faces_only, 2);
   count_launch();
   return cudaGetLastError();
 }

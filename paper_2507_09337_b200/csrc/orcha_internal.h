@@ -127,8 +127,10 @@ size_t state_bytes(const DevGrid& G, long long nslots);
 long long records_capacity(const DevGrid& G, long long nslots);
 
 // kernel launchers (kernels_*.cu); all return cudaGetLastError()
+// faces_only: 0 every guard, 1 face guards to depth 2, 2 the gather-mode
+// complement (x-guards of y/z-guard rows whose row source is remote)
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
-                        cudaStream_t s, bool faces_only = false);
+                        cudaStream_t s, int faces_only = 0);
 cudaError_t launch_fill_x(const DevGrid& G, double* state, int nslots, const NbrEntry* table, cudaStream_t s);
 cudaError_t launch_pack(const DevGrid& G, double* state, const double* staged, int nslots,
                         bool to_state, cudaStream_t s);

@@ -204,6 +204,9 @@ struct FillPlan {
   std::vector<NbrEntry*> d_cross_u1;
   CommPlan* remote = nullptr;        // guard cells sourced from other ranks (comm.cu)
   bool has_remote = false;
+  // gather mode with remote sources: some y/z-guard row of the packet has a
+  // remote source while one of its x-guard parts has a resident one
+  std::vector<char> edge_fix;
 };
 static std::mutex g_plan_mu;
 static std::vector<FillPlan*> g_plans;
@@ -490,6 +493,13 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     }
     f->d_tables.push_back(d);
     f->d_tables_u1.push_back(d1);
+    char fix = 0;
+    for (int s = 0; s < p->nslots && !fix; s++)
+      for (int dd = 0; dd < 27; dd++) {
+        const int ox = dd % 3 - 1, row = dd - (ox + 1) + 1;  // (0, oy, oz) of the same row
+        if (ox != 0 && row != 13 && !tab[(size_t)s * 27 + row].src && tab[(size_t)s * 27 + dd].src) fix = 1;
+      }
+    f->edge_fix.push_back(fix);
     // push tables: target of direction o = make_entry(b, o).src_block (the
     // neighbour at b+o, or b itself across a clamp/mirror boundary)
     std::vector<PushEntry> pt((size_t)p->nslots * 27), pt1;
@@ -613,18 +623,25 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   bool all_pushed = push_enabled();
   for (int q = 0; q < npk; q++)
     all_pushed &= pk[q]->push_plan == f && (buffer ? pk[q]->u1_pushed : pk[q]->guards_pushed);
-  // gather mode (state only, fused kernels, ONE packet with every source
-  // resident): x-guards only.  With several packets the advances run one after
+  // gather mode (state only, fused kernels, ONE packet per device; remote
+  // sources were exchanged into its own guards above): x-guards only, plus
+  // the resident-sourced parts of exchanged rows.  With several packets the advances run one after
   // another and a later packet's stage 1 would read a neighbour packet's
   // already-advanced interior, so multi-packet sets keep the full fill; so
   // does the guard-push mode (its kernels have no gather staging).
   const DevGrid& G0 = pk[0]->grid->dev;
-  const bool xonly = buffer == 0 && npk == 1 && !push_enabled() && fill_mode() == 1 && !f->has_remote &&
+  const bool xonly = buffer == 0 && npk == 1 && !push_enabled() && fill_mode() == 1 &&
                      kernel_variant() == 1 && fused_supported(G0);
   for (int q = 0; q < npk; q++) {
     double* dst = buffer ? pk[q]->scratch : pk[q]->state;
     cudaError_t e;
     if (xonly) {
+      // rows with a remote source were exchanged into our guards: their
+      // x-guard parts with resident sources are filled here
+      if (f->edge_fix[q]) {
+        e = launch_fill(G0, dst, pk[q]->nslots, f->d_tables[q], s, 2);
+        if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
+      }
       // the last advance scattered U^{n+1} into the x-guards with this plan: nothing to do
       if (pk[q]->xguards_pushed && pk[q]->push_plan == f) continue;
       e = launch_fill_x(G0, dst, pk[q]->nslots, f->d_tables[q], s);
@@ -632,7 +649,7 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
       const NbrEntry* tab = all_pushed ? (buffer ? f->d_cross_u1[q] : f->d_cross[q])   // cross-packet only
                                        : (buffer ? f->d_tables_u1[q] : f->d_tables[q]);
       if (!tab) continue;  // pushed, and no source in another packet
-      e = launch_fill(pk[q]->grid->dev, dst, pk[q]->nslots, tab, s, faces_only);
+      e = launch_fill(pk[q]->grid->dev, dst, pk[q]->nslots, tab, s, faces_only ? 1 : 0);
     }
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   }

@@ -72,6 +72,44 @@ def test_virtual_ranks_bitwise_equal_single_domain(case):
     assert np.array_equal(A, B)
 
 
+@pytest.mark.parametrize("case", CASES)
+def test_virtual_ranks_gather_mode_one_packet_per_rank(case):
+    # one packet per rank: the gather fill mode runs with remote sources (the
+    # exchange writes them into the packet's own guards, stage 1 stages the
+    # rest from the resident owners); bitwise the single-domain full fill
+    from paper_2507_09337_b200 import abi, hydro
+    ndim, nb, nblk, bc, gg, brick = case
+    g = H.make_grid(ndim, nb, nblk, bc=bc)
+    owner = hydro.brick_owner(nblk, brick, gg)
+    U0 = inp.random_field(g.N[:ndim], seed=8)
+    abi.call(g.lib, "orcha_set_fill_mode", 0)
+    try:
+        A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
+    finally:
+        abi.call(g.lib, "orcha_set_fill_mode", 1)
+    B, dts = _run_virtual(g, U0, owner, 4, packets_per_rank=1)
+    assert dts == [x[0] for x in logA]
+    assert np.array_equal(A, B)
+
+
+def test_virtual_ranks_gather_mode_scattered_owners():
+    # a non-brick owner map: some y/z-guard rows have a remote source while
+    # their x-guard parts are resident (the fill's complement pass writes those)
+    from paper_2507_09337_b200 import abi
+    g = H.make_grid(3, (8, 8, 8), (4, 3, 2), bc=((R, O), (P, P), (O, R)))
+    owner = (np.random.default_rng(4).random(g.nblocks) * 3).astype(np.int32)
+    owner[:3] = [0, 1, 2]
+    U0 = inp.random_field(g.N, seed=9)
+    abi.call(g.lib, "orcha_set_fill_mode", 0)
+    try:
+        A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
+    finally:
+        abi.call(g.lib, "orcha_set_fill_mode", 1)
+    B, dts = _run_virtual(g, U0, owner, 4, packets_per_rank=1)
+    assert dts == [x[0] for x in logA]
+    assert np.array_equal(A, B)
+
+
 def test_virtual_ranks_parity_build_equals_oracle():
     # cfg4's decomposition in miniature: 8 bricks (one Sedov octant each)
     from paper_2507_09337_b200 import hydro

@@ -13,7 +13,7 @@ h, units = r[0], r[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 per = {}
 for row in r[2:]:
-    name = row[h.index("Kernel Name")]
+    name = row[h.index("Kernel Name")].replace("(int)", "").replace("(bool)", "")
     b = 0.0
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = h.index(k)
@@ -21,6 +21,7 @@ for row in r[2:]:
     key = "stage1" if "16, 1" in name else "stage2" if "16, 2" in name else name[:40]
     per.setdefault(key, b)
 tot = per.get("stage1", 0.0) + per.get("stage2", 0.0)
-json.dump({"advance_bytes_per_launch": tot, "per_kernel_bytes": per, "source": rep,
+src = sys.argv[3] if len(sys.argv) > 3 else rep
+json.dump({"advance_bytes_per_launch": tot, "per_kernel_bytes": per, "source": src,
            "bytes_per_cell_update": tot / (4096 * 16 ** 3)}, open(out, "w"), indent=1)
 print(open(out).read())

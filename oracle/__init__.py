@@ -38,6 +38,8 @@ _LIB = os.path.join(_HERE, "liborcha_oracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
 
 OUTFLOW, PERIODIC, REFLECT = 0, 1, 2
+HLL, HLLC = 0, 1          # Riemann solver flag
+MINMOD, MC = 0, 1         # limiter flag
 TAG_CFL, TAG_CLAMP = 0, 1
 
 
@@ -61,6 +63,8 @@ class _CGrid(ctypes.Structure):
         ("gamma", ctypes.c_double),
         ("cfl", ctypes.c_double),
         ("smallp", ctypes.c_double),
+        ("riemann", ctypes.c_int32),
+        ("limiter", ctypes.c_int32),
     ]
 
 
@@ -87,6 +91,10 @@ def _load():
         lib.oracle_minmod_slope.restype = d
         lib.oracle_hll.argtypes = [g, ctypes.c_int, dp, dp, dp]
         lib.oracle_hll.restype = None
+        lib.oracle_hllc.argtypes = [g, ctypes.c_int, dp, dp, dp]
+        lib.oracle_hllc.restype = None
+        lib.oracle_mc_slope.argtypes = [d, d, d]
+        lib.oracle_mc_slope.restype = d
         lib.oracle_face_flux.argtypes = [g, ctypes.c_int, dp, dp, dp, dp, dp]
         lib.oracle_face_flux.restype = None
         lib.oracle_dt.argtypes = [g, dp, d, dp, P(ctypes.c_int64), P(ctypes.c_int32), dp]
@@ -109,6 +117,8 @@ class Grid:
     gamma: float = 1.4
     cfl: float = 0.4
     smallp: float = 1e-30
+    riemann: int = HLL                      # F4: HLL (default) or HLLC
+    limiter: int = MINMOD                   # F4: minmod (default) or MC
 
     @property
     def ndim(self) -> int:
@@ -143,6 +153,8 @@ class Grid:
         cg.gamma = self.gamma
         cg.cfl = self.cfl
         cg.smallp = self.smallp
+        cg.riemann = int(self.riemann)
+        cg.limiter = int(self.limiter)
         return cg
 
 
@@ -179,6 +191,18 @@ def sound_speed(grid: Grid, q5: Sequence[float]) -> float:
 
 def minmod_slope(qm: float, q0: float, qp: float) -> float:
     return _load().oracle_minmod_slope(qm, q0, qp)
+
+
+def mc_slope(qm: float, q0: float, qp: float) -> float:
+    return _load().oracle_mc_slope(qm, q0, qp)
+
+
+def hllc(grid: Grid, d: int, qL: Sequence[float], qR: Sequence[float]) -> np.ndarray:
+    a = np.ascontiguousarray(qL, dtype=np.float64)
+    b = np.ascontiguousarray(qR, dtype=np.float64)
+    F = np.zeros(5)
+    _load().oracle_hllc(ctypes.byref(grid.c()), d, _dp(a), _dp(b), _dp(F))
+    return F
 
 
 def hll(grid: Grid, d: int, qL: Sequence[float], qR: Sequence[float]) -> np.ndarray:

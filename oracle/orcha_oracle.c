@@ -29,6 +29,13 @@
  *     first stage", sec 6; A9, c4, c5);
  *   - CFL dt with argmax tie-break on the lowest global cell index, then the
  *     t_end clamp (A4, c7, c8).
+ * SURVEY 8(f) F4 scheme variants (grid flags; defaults are the above):
+ *   - limiter MC (monotonized central, van Leer 1977): the slope of smallest
+ *     magnitude among 2*dm, 2*dp and (dm+dp)/2 when dm, dp agree in sign, else
+ *     0 (reading c21);
+ *   - Riemann solver HLLC (Toro, "Riemann Solvers and Numerical Methods for
+ *     Fluid Dynamics", 3rd ed., sec 10.4, eqs 10.37-10.39), same wave speeds
+ *     as HLL (reading c20).
  * The "refill" mode (ghosts of U1 refilled between the stages) is the plain
  * two-refresh scheme that P:L667-668 describes before the trick; it is the
  * oracle of SURVEY 8(f) F1 and the telescoping equivalence pin.
@@ -45,6 +52,8 @@ typedef struct {
   double xmin[3], xmax[3];
   int32_t bc[3][2];   /* per axis, low/high: 0 outflow, 1 periodic, 2 reflect */
   double gamma, cfl, smallp;
+  int32_t riemann;    /* 0 HLL, 1 HLLC (F4) */
+  int32_t limiter;    /* 0 minmod, 1 MC (F4) */
 } oracle_grid;
 
 enum { BC_OUTFLOW = 0, BC_PERIODIC = 1, BC_REFLECT = 2 };
@@ -69,6 +78,7 @@ int64_t oracle_array_len(const oracle_grid* G) { return 5 * ext(G, 0) * ext(G, 1
 static int check_grid(const oracle_grid* G) {
   if (G->ndim < 1 || G->ndim > 3) return ORC_E_ARG;
   if (G->ng < 4) return ORC_E_ARG;
+  if (G->riemann < 0 || G->riemann > 1 || G->limiter < 0 || G->limiter > 1) return ORC_E_ARG;
   for (int d = 0; d < 3; d++) {
     if (d < G->ndim) {
       if (G->N[d] < G->ng) return ORC_E_ARG;
@@ -162,6 +172,19 @@ double oracle_minmod_slope(double qm, double q0, double qp) {
   return 0.0;
 }
 
+/* MC (monotonized central) slope, reading c21. */
+double oracle_mc_slope(double qm, double q0, double qp) {
+  double dm = q0 - qm;
+  double dp = qp - q0;
+  if (dm * dp > 0.0) {
+    double a = 2.0 * fabs(dm), b = 2.0 * fabs(dp), c = 0.5 * fabs(dm + dp);
+    double m = (a < b) ? a : b;
+    m = (c < m) ? c : m;
+    return copysign(m, dm);
+  }
+  return 0.0;
+}
+
 /* ------------------------------------------------ 4. HLL */
 
 static void cons_and_flux(const oracle_grid* G, int d, const double q[5], double U[5], double F[5],
@@ -202,18 +225,58 @@ void oracle_hll(const oracle_grid* G, int d, const double qL[5], const double qR
   }
 }
 
+/* HLLC (reading c20; Toro sec 10.4).  Wave speeds S_L, S_R as in HLL; the
+ * contact speed (10.37)
+ *   S* = ((p_R - p_L) + (d_L u_L - d_R u_R)) / (d_L - d_R),  d_K = rho_K (S_K - u_K);
+ * the star state (10.39), f_K = d_K / (S_K - S*),
+ *   U*_K = (f_K, f_K S* (normal), f_K v_K, f_K w_K (transverse),
+ *           f_K (E_K / rho_K + (S* - u_K) (S* + p_K / d_K)));
+ * and F*_K = F_K + S_K (U*_K - U_K) (10.38).  F = F_L if S_L >= 0, else F_R
+ * if S_R <= 0, else F*_L if S* >= 0, else F*_R. */
+void oracle_hllc(const oracle_grid* G, int d, const double qL[5], const double qR[5], double F[5]) {
+  double UL[5], FL[5], UR[5], FR[5], cL, cR;
+  cons_and_flux(G, d, qL, UL, FL, &cL);
+  cons_and_flux(G, d, qR, UR, FR, &cR);
+  double nL = qL[1 + d], nR = qR[1 + d];
+  double a = nL - cL, b = nR - cR;
+  double SL = (a < b) ? a : b;
+  double e = nL + cL, f = nR + cR;
+  double SR = (e > f) ? e : f;
+  if (SL >= 0.0) {
+    for (int k = 0; k < 5; k++) F[k] = FL[k];
+  } else if (SR <= 0.0) {
+    for (int k = 0; k < 5; k++) F[k] = FR[k];
+  } else {
+    double dL = qL[0] * (SL - nL);
+    double dR = qR[0] * (SR - nR);
+    double Ss = ((qR[4] - qL[4]) + (dL * nL - dR * nR)) / (dL - dR);
+    int left = Ss >= 0.0;
+    const double* q = left ? qL : qR;
+    const double* U = left ? UL : UR;
+    const double* FK = left ? FL : FR;
+    double SK = left ? SL : SR, dK = left ? dL : dR, nK = left ? nL : nR;
+    double fK = dK / (SK - Ss);
+    double Us[5];
+    Us[0] = fK;
+    for (int t = 0; t < 3; t++) Us[1 + t] = (t == d) ? fK * Ss : fK * q[1 + t];
+    Us[4] = fK * (U[4] / q[0] + (Ss - nK) * (Ss + q[4] / dK));
+    for (int k = 0; k < 5; k++) F[k] = FK[k] + SK * (Us[k] - U[k]);
+  }
+}
+
 /* Face flux at the face between cells i and i+1 along axis d, from the four
  * primitive states q_{i-1}, q_i, q_{i+1}, q_{i+2} (each [5]). */
 void oracle_face_flux(const oracle_grid* G, int d, const double qm[5], const double q0[5],
                       const double q1[5], const double q2[5], double F[5]) {
   double qL[5], qR[5];
   for (int v = 0; v < 5; v++) {
-    double s0 = oracle_minmod_slope(qm[v], q0[v], q1[v]);
-    double s1 = oracle_minmod_slope(q0[v], q1[v], q2[v]);
+    double s0 = G->limiter ? oracle_mc_slope(qm[v], q0[v], q1[v]) : oracle_minmod_slope(qm[v], q0[v], q1[v]);
+    double s1 = G->limiter ? oracle_mc_slope(q0[v], q1[v], q2[v]) : oracle_minmod_slope(q0[v], q1[v], q2[v]);
     qL[v] = q0[v] + 0.5 * s0;
     qR[v] = q1[v] - 0.5 * s1;
   }
-  oracle_hll(G, d, qL, qR, F);
+  if (G->riemann) oracle_hllc(G, d, qL, qR, F);
+  else oracle_hll(G, d, qL, qR, F);
 }
 
 /* --------------------------------------------------- the method on arrays */

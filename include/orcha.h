@@ -74,7 +74,16 @@ typedef struct {
   double gamma;       /* ideal-gas gamma; e.g. 1.4 */
   double cfl;         /* CFL number (reading c7); e.g. 0.4 */
   double smallp;      /* pressure floor used in primitive recovery only (c10); e.g. 1e-30 */
+  /* SURVEY 8(f) F4 scheme variants (zero = the paper-path defaults):
+   * riemann: ORCHA_RIEMANN_HLL (A7) or ORCHA_RIEMANN_HLLC (Toro sec 10.4,
+   * same wave speeds; reading c20); limiter: ORCHA_LIMITER_MINMOD
+   * (A6) or ORCHA_LIMITER_MC (monotonized central, reading c21). */
+  int32_t riemann;
+  int32_t limiter;
 } orcha_grid_desc;
+
+enum { ORCHA_RIEMANN_HLL = 0, ORCHA_RIEMANN_HLLC = 1 };
+enum { ORCHA_LIMITER_MINMOD = 0, ORCHA_LIMITER_MC = 1 };
 
 typedef struct orcha_grid orcha_grid;
 typedef struct orcha_packet orcha_packet;
@@ -93,7 +102,7 @@ typedef struct {
 
 /* Validate `desc` and create a grid handle (host only, no device work).
  * Errors: ORCHA_E_ARG (ndim, nb, nblk, extents, bc codes, gamma <= 1,
- * cfl <= 0), ORCHA_E_HALO (ng < 4), ORCHA_E_ARG if a periodic axis has fewer
+ * cfl <= 0, riemann / limiter codes), ORCHA_E_HALO (ng < 4), ORCHA_E_ARG if a periodic axis has fewer
  * cells than ng. */
 int32_t orcha_grid_create(const orcha_grid_desc* desc, orcha_grid** out);
 int32_t orcha_grid_destroy(orcha_grid* grid);

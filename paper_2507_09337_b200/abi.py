@@ -16,6 +16,8 @@ ORCHA_OK = 0
 STATUS = {0: "ORCHA_OK", -1: "ORCHA_E_ARG", -2: "ORCHA_E_RANGE", -3: "ORCHA_E_HALO", -4: "ORCHA_E_NONPHYSICAL",
           -5: "ORCHA_E_LAYOUT", -6: "ORCHA_E_CUDA", -7: "ORCHA_E_NCCL", -8: "ORCHA_E_STATE"}
 BC_OUTFLOW, BC_PERIODIC, BC_REFLECT = 0, 1, 2
+RIEMANN_HLL, RIEMANN_HLLC = 0, 1
+LIMITER_MINMOD, LIMITER_MC = 0, 1
 DT_CFL, DT_CLAMP = 0, 1
 
 EXPORTS = [
@@ -49,6 +51,8 @@ class orcha_grid_desc(ctypes.Structure):
         ("gamma", ctypes.c_double),
         ("cfl", ctypes.c_double),
         ("smallp", ctypes.c_double),
+        ("riemann", ctypes.c_int32),
+        ("limiter", ctypes.c_int32),
     ]
 
 

@@ -59,28 +59,30 @@ def _compile(src: str, obj: str, flags) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> list:
+    """Compile every translation unit of both libraries (production and
+    parity) in one pool, then link each library."""
     out = []
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
+    todo = {}
     for lib, flags in VARIANTS.items():
         target = os.path.join(HERE, lib)
         out.append(target)
-        if not force and not _stale(target):
-            continue
-        tag = os.path.splitext(lib)[0]
-        objs = []
-        with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-            futs = {}
-            for src in sources():
-                obj = os.path.join(objdir, f"{tag}_{os.path.splitext(os.path.basename(src))[0]}.o")
-                objs.append(obj)
-                futs[ex.submit(_compile, src, obj, flags)] = src
-            for f in cf.as_completed(futs):
-                msg = f.result()
-                if verbose and msg.strip():
-                    print(msg, file=sys.stderr)
+        if force or _stale(target):
+            tag = os.path.splitext(lib)[0]
+            todo[target] = (flags, [(src, os.path.join(objdir, f"{tag}_{os.path.splitext(os.path.basename(src))[0]}.o"))
+                                    for src in sources()])
+    if not todo:
+        return out
+    with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        futs = [ex.submit(_compile, src, obj, flags) for flags, pairs in todo.values() for src, obj in pairs]
+        for f in cf.as_completed(futs):
+            msg = f.result()
+            if verbose and msg.strip():
+                print(msg, file=sys.stderr)
+    for target, (flags, pairs) in todo.items():
         tmp = target + f".{os.getpid()}.tmp"
-        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[obj for _, obj in pairs], "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

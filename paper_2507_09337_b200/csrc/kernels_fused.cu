@@ -1,533 +1,24 @@
-// kernels_fused.cu -- the performance advance: per-stage fused z-marching
-// kernels (sm_100a, fp64).
-//
-// A CTA owns a band of H output rows of one block's output x-y plane (16^3
-// blocks: two bands per block, so 2-3 independent CTAs share an SM and one
-// CTA's barrier is covered by another's work) and marches over the output
-// z-planes of the stage.  Its input rows of each plane (5 variables x
-// (H+4) rows x the padded row length -- a contiguous run per variable in the
-// block-major SoA packet) are staged into a 5-deep shared-memory ring by bulk
-// async copies (cp.async.bulk -> UBLKCP, completion on an mbarrier), and
-// converted to primitives in place (EOS).  Per output plane k:
-//   phase 1: every x-, y- and z-face flux of the band is one task (PLM/minmod
-//            from the 4-cell stencil, then HLL), computed exactly once and
-//            written to shared memory; tasks are dealt in warp-sized slots of
-//            one direction (no divergence, no selects); z-faces k+1/2 are
-//            double buffered so the k-1/2 ones survive the plane;
-//   phase 2: the conservative update of the band's cells of plane k, and the
-//            EOS of the next staged plane.
-// Stage 1 (box: interior + 2-cell ring) writes U1 to an (n+4)^3 scratch;
-// stage 2 (interior) reads it, writes U^{n+1} in place and reduces the CFL
-// signal speed of the new state (fused dt epilogue).  SURVEY 8(a) A5-A9;
-// P:L665-674 sec 6.
-//
-// Expression order is that of hydro_math.cuh: the parity
-// build of this kernel is bitwise equal to the reference kernel and the
-// oracle.  The production build uses hydro_math.cuh's reciprocal / rsqrt
-// refinements instead of IEEE divide and sqrt.
-#include <cfloat>
-#include <cstdint>
-
-#include "hydro_math.cuh"
+// kernels_fused.cu -- dispatch of the fused stage kernels (fused_impl.cuh)
+// to the per-(block size, scheme) translation units kernels_fused_n*_s*.cu.
 #include "orcha_internal.h"
-#include "push.cuh"
-#include "reduce.cuh"
 
 namespace orcha {
 
-// ------------------------------------------------------------ PTX helpers --
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "ORCHA_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra ORCHA_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-
-// ------------------------------------------------------------- geometry ----
-// MODE 0 = telescoped step (stage 1 on the box interior+2, U1 in an (n+4)^3
-// scratch, no refill); MODE 1 = per-stage step (both stages
-// on the interior, U1 in a padded (n+8)^3 scratch whose guards are refilled
-// between the stages).
-template <int NB, int STAGE, int SPLIT, int MODE = 0>
-struct Geo {
-  static constexpr int W = (STAGE == 1 && MODE == 0) ? NB + 4 : NB;  // output columns (and rows) per plane
-  static constexpr int OFF = (W - NB) / 2;                   // output origin (interior-relative) = -OFF
-  static constexpr int K0 = -OFF;                            // first output plane
-  static constexpr int NK = W;                               // output planes
-  static constexpr int INO = (STAGE == 1 || MODE == 1) ? 4 : 2;  // input origin offset (guards / ring)
-  static constexpr int ORG = INO - 2 - OFF;                  // first staged padded row / plane
-  static constexpr int IPX = NB + 2 * INO;                   // padded input row length (= plane rows)
-  static constexpr int PLANE = IPX * IPX;                    // doubles per input plane per variable
-  static constexpr int NPLANES = NK + 4;                     // input planes streamed
-  static constexpr int NSPLIT = SPLIT;                       // row bands per block
-  static constexpr int H = W / NSPLIT;                       // output rows per CTA
-  static constexpr int IR = H + 4;                           // staged input rows per plane
-  static constexpr int BAND = IR * IPX;                      // doubles per staged band per variable
-  static constexpr int NS = 5;                               // ring depth
-  static constexpr int FX = H * (W + 1);                     // x-faces per band
-  static constexpr int FY = (H + 1) * W;                     // y-faces per band
-  static constexpr int FZ = H * W;                           // z-faces per band (and cells)
-  // face tasks are dealt out in warp-sized slots of one direction each; the
-  // warp count is chosen so every warp gets two slots (two rounds)
-  static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
-  static constexpr int NSLOT = SX + SY + SZ;
-  static constexpr int NW = (NB >= 16) ? (NSLOT + 1) / 2 : (W * W + 31) / 32;
-  static constexpr int NT = NW * 32;
-  static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
-  // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
-  static constexpr size_t SMEM =
-      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64 + ((NS * IR + 15) / 16) * 16;
-  // CTAs per SM we aim for: shared memory bound (227 KB per SM), at most 4
-  static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
-  static constexpr int MINB = MINB_S < 1 ? 1 : (MINB_S > 4 ? 4 : MINB_S);
-  static_assert(NT >= FZ, "one update cell per thread");
-  static_assert((BAND * 8) % 16 == 0, "bulk copies need 16-byte multiples");
-};
-
-// Interior coordinate whose value the guard coordinate c (side o = -1/0/+1
-// of an axis of NB cells) takes under neighbour-table mode m.
-template <int NB>
-__device__ __forceinline__ int guard_image(int c, int o, int m) {
-  return o == 0 ? c : m == kShift ? c - o * NB : m == kClamp ? (o < 0 ? 0 : NB - 1) : (o < 0 ? -1 - c : 2 * NB - 1 - c);
-}
-
-// U1 scratch of the fused path: per (slot, var) an (n+4)^3 cube (origin -2),
-// 256-byte aligned.
-template <int NB>
-__host__ __device__ constexpr long long u1_cube() {
-  return ((long long)(NB + 4) * (NB + 4) * (NB + 4) * 8 + 255) / 256 * 256 / 8;
-}
-
-// PUSH: 0 none, 1 scatter the new state into every same-packet guard
-// (push_cell), 2 into the x-guards only (push_cell_x, gather mode).
-// GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a
-// separate instantiation so the plain kernels carry none of its registers.
-template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER>
-__global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
-    stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
-                       const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
-                       DtRecord* __restrict__ rec, DevStatus* st, const PushEntry* __restrict__ push,
-                       const NbrEntry* __restrict__ nbr) {
-  using Gm = Geo<NB, STAGE, SPLIT, MODE>;
-  constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
-  constexpr int NT = Gm::NT, H = Gm::H, ORG = Gm::ORG;
-  // U1 cube stride: (n+4)^3 compact scratch (telescoped) or the padded state layout (per-stage)
-  const long long U1C = (MODE == 0) ? u1_cube<NB>() : G.cube;
-  auto u1_off = [&](int ci, int cj, int k) -> long long {
-    return (MODE == 0) ? ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2) : cell_off(G, ci, cj, k);
-  };
-  extern __shared__ __align__(128) double smem[];
-  double* ring = smem;                                   // [NS][5][IR][IPX]
-  double* Fx = ring + NS * 5 * BAND;                     // [5][H][W+1]
-  double* Fy = Fx + 5 * Gm::FX;                          // [5][H+1][W]
-  double* Fz = Fy + 5 * Gm::FY;                          // [2][5][H][W]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Fz + 2 * 5 * Gm::FZ);
-  unsigned char* flipm = reinterpret_cast<unsigned char*>(bar + 8);  // [NS][IR]
-
-  const int tid = threadIdx.x;
-  const long long slot = blockIdx.x / Gm::NSPLIT;
-  const int band = blockIdx.x % Gm::NSPLIT;
-  const int jj0 = band * H;                              // first output row of the band (0-based)
-  const long long cube = G.cube;
-  const double dt = d_dt ? *d_dt : h_dt;
-  const double* in = (STAGE == 1) ? state + slot * 5 * cube : u1 + slot * 5 * U1C;
-  const long long in_cube = (STAGE == 1) ? cube : U1C;
-  const SlotInfo si = slots[slot];
-
-  __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
-  if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
-  __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
-  if (STAGE == 1 && GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
-  if (tid == 0) {
-    for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  // input plane p (0-based, z = K0 - 2 + p): padded rows [jj0, jj0 + IR) -> ring slot p % NS.
-  // Called by warp 0 (all lanes) after a CTA barrier that follows every
-  // generic access to the slot; the proxy fence of each issuing lane orders
-  // those before its async copies.
-  auto issue = [&](int p) {
-    if (p < Gm::NPLANES) {
-      const int s = p % NS, lane = tid & 31;
-      if (STAGE == 1 && GATHER) {
-        // Gather mode: only the x-guards were filled.  Each staged row
-        // (padded plane pp, padded row pr) is the (y, z) image of a row of
-        // the block that owns it -- the neighbour table's (0, oy, oz) entry --
-        // whose x-guards are filled: the axis-ordered ghost fill composed on
-        // the fly (x, then y over x-guards, then z over x,y-guards).  Lane r
-        // resolves row r; rows whose sources are consecutive form one copy,
-        // issued by the lane that starts the run.
-        const int pp = p + ORG, z = pp - INO;
-        const int oz = z < 0 ? -1 : (z >= NB ? 1 : 0);
-        const double* rp = nullptr;
-        int fl = 0;
-        if (lane < Gm::IR) {
-          const int pr = jj0 + ORG + lane, y = pr - INO;
-          const int oy = y < 0 ? -1 : (y >= NB ? 1 : 0);
-          const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
-          if (e.src == nullptr) {  // remote source: its rows were exchanged into our own guards
-            rp = in + (long long)pp * Gm::PLANE + (long long)pr * IPX;
-          } else {
-            const int ys = guard_image<NB>(y, oy, (e.mode >> 2) & 3), zs = guard_image<NB>(z, oz, (e.mode >> 4) & 3);
-            rp = e.src + (long long)(zs + INO) * Gm::PLANE + (long long)(ys + INO) * IPX;
-            fl = e.flip & 0xC;  // mirrored y -> negate rho*v (bit 2), z -> rho*w (bit 3)
-          }
-          flipm[s * Gm::IR + lane] = (unsigned char)fl;
-        }
-        const double* prev = (const double*)__shfl_up_sync(0xffffffffu, (unsigned long long)rp, 1);
-        const int pfl = __shfl_up_sync(0xffffffffu, fl, 1);
-        const bool start = lane < Gm::IR && (lane == 0 || rp != prev + IPX || fl != pfl);
-        const unsigned starts = __ballot_sync(0xffffffffu, start);
-        if (lane == 0) mbar_expect_tx(&bar[s], 5u * BAND * 8u);
-        __syncwarp();
-        if (start) {
-          const unsigned later = starts & ~((2u << lane) - 1u);
-          const int run = (later ? __ffs(later) - 1 : Gm::IR) - lane;
-          fence_proxy_async();
-#pragma unroll
-          for (int v = 0; v < 5; v++)
-            bulk_load(ring + (s * 5 + v) * BAND + lane * IPX, rp + v * in_cube, (uint32_t)(run * IPX * 8), &bar[s]);
-        }
-      } else if (lane == 0) {
-        fence_proxy_async();
-        mbar_expect_tx(&bar[s], 5u * BAND * 8u);
-#pragma unroll
-        for (int v = 0; v < 5; v++)
-          bulk_load(ring + (s * 5 + v) * BAND,
-                    in + v * in_cube + (long long)(p + ORG) * Gm::PLANE + (long long)(jj0 + ORG) * IPX, BAND * 8u,
-                    &bar[s]);
-      }
-    }
-  };
-  auto wait_plane = [&](int p) { mbar_wait(&bar[p % NS], (p / NS) & 1); };
-  auto convert = [&](int p) {  // EOS in place over the staged band of plane p
-    double* Q = ring + (p % NS) * 5 * BAND;
-    const int z = Gm::K0 - 2 + p;
-    unsigned long long hits = 0;
-    for (int c = tid; c < BAND; c += NT) {
-      bool fl;
-      int r = c / IPX;
-      double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
-      if (STAGE == 1 && GATHER) {  // gather mode: mirrored guard rows negate rho*v / rho*w
-        const unsigned fm = flipm[(p % NS) * Gm::IR + r];
-        if (fm & 4) my = -my;
-        if (fm & 8) mz = -mz;
-      }
-      Prim q = eos(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl);
-      int x = c - r * IPX - INO, y = jj0 + ORG + r - INO;
-      // own (non-overlapping) rows of the band only, so each cell counts once
-      bool mine = r >= 2 && r < 2 + H;
-      if (mine && x >= 0 && x < NB && y >= 0 && y < NB && z >= 0 && z < NB) {
-        hits += fl ? 1 : 0;
-        if (STAGE == 1 && !(q.r > 0.0)) {
-          long long g = (((long long)si.bc[2] * NB + z) * G.N[1] + ((long long)si.bc[1] * NB + y)) * G.N[0] +
-                        ((long long)si.bc[0] * NB + x);
-          atomicMin(&st->first_bad, (unsigned long long)g);
-        }
-      }
-      Q[c] = q.r;
-      Q[BAND + c] = q.u;
-      Q[2 * BAND + c] = q.v;
-      Q[3 * BAND + c] = q.w;
-      Q[4 * BAND + c] = q.p;
-    }
-    if (hits) atomicAdd(&st->floor_hits, hits);
-  };
-  auto ld = [&](const double* P, int o, Prim& q) {
-    q.r = P[o];
-    q.u = P[BAND + o];
-    q.v = P[2 * BAND + o];
-    q.w = P[3 * BAND + o];
-    q.p = P[4 * BAND + o];
-  };
-  // band-local output row j (0..H) <-> staged row j + 2; output column i <-> staged column i - OFF + INO
-  // x-face between columns f-1 and f of band row j
-  // stencil base offset (in a staged band) of face task t of direction kind
-  auto task_base = [&](int kind, int t) -> int {
-    if (kind == 0) {
-      int j = t / (W + 1), f = t - j * (W + 1);
-      return (j + 2) * IPX + (f - OFF - 2 + INO);
-    }
-    if (kind == 1) {
-      int f = t / W, i = t - f * W;
-      return f * IPX + (i - OFF + INO);
-    }
-    int j = t / W, i = t - j * W;
-    return (j + 2) * IPX + (i - OFF + INO);
-  };
-  auto x_task = [&](int t, int base, int it) {
-    const double* P = ring + ((it + 2) % NS) * 5 * BAND;
-    Prim q0, q1, q2, q3, L, R;
-    ld(P, base, q0);
-    ld(P, base + 1, q1);
-    ld(P, base + 2, q2);
-    ld(P, base + 3, q3);
-    plm_face(q0, q1, q2, q3, &L, &R);
-    hll_store<0>(L, R, G, Fx + t, Gm::FX);
-  };
-  // y-face between band rows f-1 and f of column i
-  auto y_task = [&](int u, int base, int it) {
-    const double* P = ring + ((it + 2) % NS) * 5 * BAND;
-    Prim q0, q1, q2, q3, L, R;
-    ld(P, base, q0);
-    ld(P, base + IPX, q1);
-    ld(P, base + 2 * IPX, q2);
-    ld(P, base + 3 * IPX, q3);
-    plm_face(q0, q1, q2, q3, &L, &R);
-    hll_store<1>(L, R, G, Fy + u, Gm::FY);
-  };
-  // z-face k+1/2 of column (i, j): stencil planes it+1 .. it+4 (z = k-1 .. k+2)
-  auto z_task = [&](int w, int base, int it, double* fz_out) {
-    Prim q0, q1, q2, q3, L, R;
-    ld(ring + ((it + 1) % NS) * 5 * BAND, base, q0);
-    ld(ring + ((it + 2) % NS) * 5 * BAND, base, q1);
-    ld(ring + ((it + 3) % NS) * 5 * BAND, base, q2);
-    ld(ring + ((it + 4) % NS) * 5 * BAND, base, q3);
-    plm_face(q0, q1, q2, q3, &L, &R);
-    hll_store<2>(L, R, G, fz_out + w, Gm::FZ);
-  };
-  const int warp = tid >> 5, lane = tid & 31;
-  // this thread's face tasks (the same on every plane): warp-uniform direction
-  // slots r*NW + warp, decoded once
-  int tkind[Gm::ROUNDS], ttask[Gm::ROUNDS], tbase[Gm::ROUNDS];
-#pragma unroll
-  for (int r = 0; r < Gm::ROUNDS; r++) {
-    const int m = r * Gm::NW + warp;
-    int kind = 3, t = 0;
-    if (m < Gm::SX) { t = m * 32 + lane; kind = t < Gm::FX ? 0 : 3; }
-    else if (m < Gm::SX + Gm::SY) { t = (m - Gm::SX) * 32 + lane; kind = t < Gm::FY ? 1 : 3; }
-    else if (m < Gm::NSLOT) { t = (m - Gm::SX - Gm::SY) * 32 + lane; kind = t < Gm::FZ ? 2 : 3; }
-    tkind[r] = kind;
-    ttask[r] = t;
-    tbase[r] = kind < 3 ? task_base(kind, t) : 0;
-  }
-
-  // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
-  if (tid < 32)
-    for (int p = 0; p < NS; p++) issue(p);
-  if (STAGE == 1 && GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
-  for (int p = 0; p < 5; p++) {
-    wait_plane(p);
-    convert(p);
-  }
-  __syncthreads();
-  for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
-  __syncthreads();
-  if (tid < 32) issue(5);  // into the slot of plane 0
-
-  double s_rec = -DBL_MAX;
-  long long g_rec = LLONG_MAX;
-#pragma unroll 1
-  for (int it = 0; it < Gm::NK; it++) {
-    const int k = Gm::K0 + it;
-    // prefetch the update operands of this thread's cell of plane k
-    const bool upd = tid < Gm::FZ;
-    const int lj = upd ? tid / W : 0, li = upd ? tid - (tid / W) * W : 0;
-    const int ci = li - OFF, cj = jj0 + lj - OFF;
-    const long long so = cell_off(G, ci, cj, k);
-    double un[5], v1[5];
-    if (upd) {
-      const double* ub = state + slot * 5 * cube;
-      long long uo = so;
-      int ufl = 0;
-      if (STAGE == 1 && MODE == 0 && GATHER) {
-        // gather mode: the box's y/z guard-ring cells were not filled; U^n of
-        // such a cell is its image in the owning block (x-guards are filled)
-        const int oy = cj < 0 ? -1 : (cj >= NB ? 1 : 0), oz = k < 0 ? -1 : (k >= NB ? 1 : 0);
-        if (oy != 0 || oz != 0) {
-          const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
-          if (e.src != nullptr) {
-            ub = e.src;
-            uo = cell_off(G, ci, guard_image<NB>(cj, oy, (e.mode >> 2) & 3), guard_image<NB>(k, oz, (e.mode >> 4) & 3));
-            ufl = e.flip & 0xC;
-          }
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < 5; v++) un[v] = __ldg(ub + v * cube + uo);
-      if (ufl & 4) un[2] = -un[2];
-      if (ufl & 8) un[3] = -un[3];
-      if (STAGE == 2) {
-        const long long uo = u1_off(ci, cj, k);
-#pragma unroll
-        for (int v = 0; v < 5; v++) v1[v] = __ldg(u1 + slot * 5 * U1C + v * U1C + uo);
-      }
-    }
-    // phase 1: all face fluxes of the band's plane k (inputs: planes it+1 .. it+4)
-    double* fz_cur = Fz + (it & 1) * 5 * Gm::FZ;
-#pragma unroll
-    for (int r = 0; r < Gm::ROUNDS; r++) {
-      if (tkind[r] == 0) x_task(ttask[r], tbase[r], it);
-      else if (tkind[r] == 1) y_task(ttask[r], tbase[r], it);
-      else if (tkind[r] == 2) z_task(ttask[r], tbase[r], it, fz_cur);
-    }
-    __syncthreads();
-    // phase 2: stage plane it+6 into the slot of plane it+1 (read for the
-    // last time in phase 1), convert plane it+5, update the band's cells
-    if (tid < 32) issue(it + 6);
-    if (it + 5 < Gm::NPLANES) {
-      wait_plane(it + 5);
-      convert(it + 5);
-    }
-    if (upd) {
-      const double* fz_prev = Fz + ((it + 1) & 1) * 5 * Gm::FZ;
-      double D[5];
-#pragma unroll
-      for (int v = 0; v < 5; v++) {
-        double tx = (Fx[v * Gm::FX + lj * (W + 1) + li + 1] - Fx[v * Gm::FX + lj * (W + 1) + li]) * G.id[0];
-        double ty = (Fy[v * Gm::FY + (lj + 1) * W + li] - Fy[v * Gm::FY + lj * W + li]) * G.id[1];
-        double tz = (fz_cur[v * Gm::FZ + tid] - fz_prev[v * Gm::FZ + tid]) * G.id[2];
-        D[v] = (tx + ty) + tz;
-      }
-      if (STAGE == 1) {
-        double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
-#pragma unroll
-        for (int v = 0; v < 5; v++) out[v * U1C] = un[v] - dt * D[v];
-        if (MODE == 1 && PUSH) {  // per-stage: scatter U1 into the U1 guards of the neighbours
-          double w[5];
-#pragma unroll
-          for (int v = 0; v < 5; v++) w[v] = un[v] - dt * D[v];
-          push_cell(G, push + slot * 27, ci, cj, k, w);
-        }
-      } else {
-        double nw[5];
-#pragma unroll
-        for (int v = 0; v < 5; v++) nw[v] = 0.5 * (un[v] + (v1[v] - dt * D[v]));
-        double* dst = state + slot * 5 * cube + so;
-#pragma unroll
-        for (int v = 0; v < 5; v++) dst[v * cube] = nw[v];
-        if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
-        if (PUSH == 2) {  // x-guards only (the x-axis part of push_cell; both entries cached in shared memory)
-          const int side = ci >= NB - 4 ? 1 : (ci < 4 ? 0 : -1);
-          if (side >= 0 && sxp[side].dst != nullptr) {
-            const PushEntry e = sxp[side];
-            const int m = e.mode & 3;
-            int t0, cnt = 1;
-            if (m == kShift) t0 = side ? ci - NB : ci + NB;
-            else if (m == kMirror) t0 = side ? 2 * NB - 1 - ci : -1 - ci;
-            else { cnt = (side ? ci == NB - 1 : ci == 0) ? 4 : 0; t0 = side ? NB : -4; }
-            for (int xx = 0; xx < cnt; xx++) {
-              double* q = e.dst + cell_off(G, t0 + xx, cj, k);
-#pragma unroll
-              for (int v = 0; v < 5; v++) q[v * cube] = ((e.flip >> v) & 1) ? -nw[v] : nw[v];
-            }
-          }
-        }
-        bool f2;
-        Prim q = eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
-        double s = signal_speed<3>(q, G);
-        long long g = (((long long)si.bc[2] * NB + k) * G.N[1] + ((long long)si.bc[1] * NB + cj)) * G.N[0] +
-                      ((long long)si.bc[0] * NB + ci);
-        if (dt_better(s, g, s_rec, g_rec)) { s_rec = s; g_rec = g; }
-        bool finite = isfinite(nw[0]) && isfinite(nw[1]) && isfinite(nw[2]) && isfinite(nw[3]) && isfinite(nw[4]);
-        if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)g);
-      }
-    }
-    __syncthreads();
-  }
-  if (STAGE == 2) {
-    block_reduce_rec<NT>(s_rec, g_rec);
-    if (tid == 0) { rec[blockIdx.x].s = s_rec; rec[blockIdx.x].g = g_rec; }
-  }
-}
-template <int NB, int STAGE, int SPLIT, int MODE>
-static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
-                         const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s,
-                         const PushEntry* push = nullptr, const NbrEntry* nbr = nullptr, int pushkind = 1) {
-  using Gm = Geo<NB, STAGE, SPLIT, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    const int sm = (int)Gm::SMEM;
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (STAGE == 1)
-      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (STAGE == 2 && MODE == 0)
-      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    attr = true;
-  }
-  // the guard-push epilogues and the gather staging are separate
-  // instantiations so the default kernels carry none of their registers
-  const dim3 grid(nslots * SPLIT);
-  if (push && pushkind == 2) {
-    if constexpr (STAGE == 2 && MODE == 0)
-      stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false><<<grid, Gm::NT, Gm::SMEM, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr);
-  } else if (push) {
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false><<<grid, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr);
-  } else if (nbr) {
-    if constexpr (STAGE == 1)
-      stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true><<<grid, Gm::NT, Gm::SMEM, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nbr);
-  } else {
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false><<<grid, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nullptr);
-  }
-  count_launch();
-}
-
-// Row bands per block (CTAs per block) for 16^3: measured best by default;
-// ORCHA_SPLIT1 / ORCHA_SPLIT2 (2 or 4) override for experiments.
-static int split_env(const char* name, int dflt) {
-  const char* e = getenv(name);
-  if (!e) return dflt;
-  int v = atoi(e);
-  return (v == 2 || v == 4) ? v : dflt;
-}
-
-template <int NB>
-static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
-                             const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
-                             cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk) {
-  int s2 = 1;
-  if constexpr (NB == 16) {
-    static const int s1 = split_env("ORCHA_SPLIT1", 2);
-    static const int s2v = split_env("ORCHA_SPLIT2", 2);
-    s2 = s2v;
-    if (s1 == 4) launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    else launch_stage<NB, 1, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    if (s2 == 4) launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
-    else launch_stage<NB, 2, 2, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
-  } else if constexpr (NB == 32) {
-    launch_stage<NB, 1, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    launch_stage<NB, 2, 4, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
-    s2 = 4;
-  } else {
-    launch_stage<NB, 1, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    launch_stage<NB, 2, 1, 0>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
-  }
-  *nrecords = (long long)nslots * s2;
-  return cudaGetLastError();
-}
+#define ORCHA_FUSED_DECL(NB, SCH)                                                                                \
+  cudaError_t fused_advance_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,             \
+                                           const SlotInfo* slots, const double* d_dt, double h_dt,              \
+                                           DtRecord* records, long long* nrecords, DevStatus* st,               \
+                                           cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk); \
+  cudaError_t fused_stage_n##NB##_s##SCH(const DevGrid& G, int stage, double* state, double* u1, int nslots,    \
+                                         const SlotInfo* slots, const double* d_dt, double h_dt,                \
+                                         DtRecord* records, long long* nrecords, DevStatus* st,                 \
+                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr);
+ORCHA_FUSED_DECL(8, 0)
+ORCHA_FUSED_DECL(8, 1)
+ORCHA_FUSED_DECL(16, 0)
+ORCHA_FUSED_DECL(16, 1)
+ORCHA_FUSED_DECL(32, 0)
+ORCHA_FUSED_DECL(32, 1)
 
 cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
@@ -557,11 +48,15 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
   const int pk = push_x_only ? 2 : 1;
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  if (G.nb[0] == 16)
-    return launch_nb<16>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk);
-  if (G.nb[0] == 32)
-    return launch_nb<32>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk);
-  return launch_nb<8>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk);
+  // the F4 scheme variants (HLLC, MC) run their own instantiations (scheme 1)
+  // so the paper-path kernels keep their register allocation
+  const bool var = G.riemann != 0 || G.limiter != 0;
+#define ORCHA_ADV(NB, SCH) \
+  fused_advance_n##NB##_s##SCH(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk)
+  if (G.nb[0] == 16) return var ? ORCHA_ADV(16, 1) : ORCHA_ADV(16, 0);
+  if (G.nb[0] == 32) return var ? ORCHA_ADV(32, 1) : ORCHA_ADV(32, 0);
+  return var ? ORCHA_ADV(8, 1) : ORCHA_ADV(8, 0);
+#undef ORCHA_ADV
 }
 
 // One stage of the per-stage variant (F1): stage 1 -> U1 (padded, interior
@@ -575,20 +70,13 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
   if (!fused_supported(G))
     return launch_stage_ref(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   const NbrEntry* n1 = (stage == 1) ? nbr : nullptr;
-  if (G.nb[0] == 16) {
-    if (stage == 1) launch_stage<16, 1, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, n1);
-    else launch_stage<16, 2, 2, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
-    if (stage == 2) *nrecords = (long long)nslots * 2;
-  } else if (G.nb[0] == 32) {
-    if (stage == 1) launch_stage<32, 1, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, n1);
-    else launch_stage<32, 2, 4, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
-    if (stage == 2) *nrecords = (long long)nslots * 4;
-  } else {
-    if (stage == 1) launch_stage<8, 1, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, n1);
-    else launch_stage<8, 2, 1, 1>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
-    if (stage == 2) *nrecords = (long long)nslots;
-  }
-  return cudaGetLastError();
+  const bool var = G.riemann != 0 || G.limiter != 0;
+#define ORCHA_STG(NB, SCH) \
+  fused_stage_n##NB##_s##SCH(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, n1)
+  if (G.nb[0] == 16) return var ? ORCHA_STG(16, 1) : ORCHA_STG(16, 0);
+  if (G.nb[0] == 32) return var ? ORCHA_STG(32, 1) : ORCHA_STG(32, 0);
+  return var ? ORCHA_STG(8, 1) : ORCHA_STG(8, 0);
+#undef ORCHA_STG
 }
 
 }  // namespace orcha

@@ -31,10 +31,12 @@ __device__ __forceinline__ void accumulate_axis(const double* __restrict__ in, l
   }
   Prim L, R;
   double Fm[5], Fp[5];
-  plm_face(q[0], q[1], q[2], q[3], &L, &R);  // face c-1/2
-  hll<AX>(L, R, G, Fm);
-  plm_face(q[1], q[2], q[3], q[4], &L, &R);  // face c+1/2
-  hll<AX>(L, R, G, Fp);
+  plm_face_var(q[0], q[1], q[2], q[3], G, &L, &R);  // face c-1/2
+  if (G.riemann == 1) hllc_store<AX>(L, R, G, Fm, 1);
+  else hll<AX>(L, R, G, Fm);
+  plm_face_var(q[1], q[2], q[3], q[4], G, &L, &R);  // face c+1/2
+  if (G.riemann == 1) hllc_store<AX>(L, R, G, Fp, 1);
+  else hll<AX>(L, R, G, Fp);
 #pragma unroll
   for (int v = 0; v < 5; v++) {
     double t = (Fp[v] - Fm[v]) * G.id[AX];

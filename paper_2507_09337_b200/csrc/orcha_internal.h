@@ -30,6 +30,7 @@ struct DevGrid {
   long long cube;   // doubles between consecutive (slot, var) cubes
   double id[3];     // 1/dx per axis (1/dx computed once)
   double gamma, gm1, ig1, cfl, smallp;  // gm1 = gamma - 1, ig1 = 1/(gamma - 1)
+  int riemann, limiter;                 // F4 scheme flags (0 = HLL / minmod)
 };
 
 // One entry per (slot, neighbour direction); 27 per slot, dir = (oz+1)*9 + (oy+1)*3 + (ox+1).

@@ -138,6 +138,8 @@ extern "C" int32_t orcha_grid_create(const orcha_grid_desc* d, orcha_grid** out)
     }
   }
   if (!(d->gamma > 1.0) || !(d->cfl > 0.0) || !(d->smallp >= 0.0)) return fail(ORCHA_E_ARG, "bad gamma/cfl/smallp");
+  if (d->riemann < 0 || d->riemann > 1 || d->limiter < 0 || d->limiter > 1)
+    return fail(ORCHA_E_ARG, "riemann must be ORCHA_RIEMANN_HLL/HLLC and limiter ORCHA_LIMITER_MINMOD/MC");
   orcha_grid* g = new orcha_grid();
   g->desc = *d;
   DevGrid& G = g->dev;
@@ -159,6 +161,8 @@ extern "C" int32_t orcha_grid_create(const orcha_grid_desc* d, orcha_grid** out)
   G.gamma = d->gamma;
   G.gm1 = d->gamma - 1.0;
   G.ig1 = 1.0 / (d->gamma - 1.0);
+  G.riemann = d->riemann;
+  G.limiter = d->limiter;
   G.cfl = d->cfl;
   G.smallp = d->smallp;
   *out = g;

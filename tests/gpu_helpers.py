@@ -10,17 +10,19 @@ import oracle
 import orcha_inputs as inp
 
 
-def make_grid(ndim, nb, nblk, bc=None, xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), parity=False):
+def make_grid(ndim, nb, nblk, bc=None, xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), parity=False, riemann=0,
+              limiter=0):
     from paper_2507_09337_b200 import hydro
     bc = bc or ((0, 0),) * 3
-    return hydro.Grid(ndim, nb, nblk, bc=bc, xmin=xmin, xmax=xmax, parity=parity)
+    return hydro.Grid(ndim, nb, nblk, bc=bc, xmin=xmin, xmax=xmax, parity=parity, riemann=riemann, limiter=limiter)
 
 
 def oracle_grid(g) -> oracle.Grid:
     nd = g.ndim
     return oracle.Grid(N=tuple(g.N[:nd]), xmin=tuple(g.desc.xmin[:nd]) + (0.0,) * (3 - nd),
                        xmax=tuple(g.desc.xmax[:nd]) + (1.0,) * (3 - nd),
-                       bc=tuple((g.desc.bc[a][0], g.desc.bc[a][1]) for a in range(3)))
+                       bc=tuple((g.desc.bc[a][0], g.desc.bc[a][1]) for a in range(3)),
+                       riemann=g.riemann, limiter=g.limiter)
 
 
 def split_packets(nblocks: int, npackets: int, seed: int = 0, shuffle: bool = False):

@@ -212,6 +212,16 @@ struct FillPlan {
   // remote source while one of its x-guard parts has a resident one
   std::vector<char> edge_fix;
 };
+// Frees a plan's device tables and the plan (not its packets' pointers).
+static void free_plan_tables(FillPlan* f) {
+  for (auto* t : f->d_tables) cudaFree(t);
+  for (auto* t : f->d_tables_u1) cudaFree(t);
+  for (auto* t : f->d_push) cudaFree(t);
+  for (auto* t : f->d_push_u1) cudaFree(t);
+  for (auto* t : f->d_cross) cudaFree(t);
+  for (auto* t : f->d_cross_u1) cudaFree(t);
+  delete f;
+}
 static std::mutex g_plan_mu;
 static std::vector<FillPlan*> g_plans;
 
@@ -222,16 +232,10 @@ static void drop_plans_with(orcha_packet* p) {
     bool hit = false;
     for (auto* q : f->packets) hit |= (q == p);
     if (hit) {
-      for (auto* t : f->d_tables) cudaFree(t);
-      for (auto* t : f->d_tables_u1) cudaFree(t);
-      for (auto* t : f->d_push) cudaFree(t);
-      for (auto* t : f->d_push_u1) cudaFree(t);
-      for (auto* t : f->d_cross) cudaFree(t);
-      for (auto* t : f->d_cross_u1) cudaFree(t);
       for (auto* q : f->packets)
         if (q->push_plan == f) { q->push_plan = nullptr; q->d_push = q->d_push_u1 = nullptr; }
       comm_free_plan(f->remote);
-      delete f;
+      free_plan_tables(f);
       g_plans.erase(g_plans.begin() + i);
     } else {
       i++;
@@ -454,9 +458,7 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
             auto it = where.find(h.src_block);
             if (it == where.end()) {
               if (!comm) {
-                for (auto* t : f->d_tables) cudaFree(t);
-                for (auto* t : f->d_tables_u1) cudaFree(t);
-                delete f;
+                free_plan_tables(f);
                 return fail(ORCHA_E_RANGE, "neighbour block " + std::to_string(h.src_block) +
                                                " is not resident on this device and no communicator was given");
               }
@@ -488,11 +490,9 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     if (err == cudaSuccess) err = cudaMalloc(&d1, tab1.size() * sizeof(NbrEntry));
     if (err == cudaSuccess) err = cudaMemcpy(d1, tab1.data(), tab1.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
     if (err != cudaSuccess) {
-      for (auto* t : f->d_tables) cudaFree(t);
-      for (auto* t : f->d_tables_u1) cudaFree(t);
       cudaFree(d);
       cudaFree(d1);
-      delete f;
+      free_plan_tables(f);
       return cuda_fail(err, "upload neighbour table");
     }
     f->d_tables.push_back(d);
@@ -544,7 +544,12 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     if (err == cudaSuccess) err = cudaMemcpy(dp, pt.data(), pt.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
     if (err == cudaSuccess) err = cudaMalloc(&dp1, pt1.size() * sizeof(PushEntry));
     if (err == cudaSuccess) err = cudaMemcpy(dp1, pt1.data(), pt1.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
-    if (err != cudaSuccess) return cuda_fail(err, "upload push table");  // (tables freed with the plan)
+    if (err != cudaSuccess) {
+      cudaFree(dp);
+      cudaFree(dp1);
+      free_plan_tables(f);
+      return cuda_fail(err, "upload push table");
+    }
     f->d_push.push_back(dp);
     f->d_push_u1.push_back(dp1);
     // cross-packet gather tables: only the directions whose source block lives
@@ -577,7 +582,12 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
       if (err == cudaSuccess) err = cudaMemcpy(dx, xc.data(), xc.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
       if (err == cudaSuccess) err = cudaMalloc(&dx1, xc1.size() * sizeof(NbrEntry));
       if (err == cudaSuccess) err = cudaMemcpy(dx1, xc1.data(), xc1.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
-      if (err != cudaSuccess) return cuda_fail(err, "upload cross-packet table");
+      if (err != cudaSuccess) {
+        cudaFree(dx);
+        cudaFree(dx1);
+        free_plan_tables(f);
+        return cuda_fail(err, "upload cross-packet table");
+      }
     }
     f->d_cross.push_back(dx);
     f->d_cross_u1.push_back(dx1);

@@ -104,6 +104,73 @@ cudaError_t launch_fill_x(const DevGrid& G, double* state, int nslots, const Nbr
   return cudaGetLastError();
 }
 
+// Every slot of several packets in one launch: slot (slot0 + blockIdx.y)'s
+// cube base and its 27 table entries come from sf (one slot per grid row, so
+// the descriptor load is uniform across the CTA); same per-cell code as
+// fill_kernel.
+__global__ void __launch_bounds__(256) fill_multi_kernel(DevGrid G, const SlotFill* __restrict__ sf,
+                                                         long long slot0, int faces_only) {
+  const long long cells = (long long)G.P[0] * G.P[1] * G.P[2];
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const long long slot = slot0 + blockIdx.y;
+  int pi = (int)(c % G.P[0]);
+  int pj = (int)((c / G.P[0]) % G.P[1]);
+  int pk = (int)(c / ((long long)G.P[0] * G.P[1]));
+  int l[3] = {pi - G.gd[0], pj - G.gd[1], pk - G.gd[2]};
+  int o[3];
+#pragma unroll
+  for (int d = 0; d < 3; d++) o[d] = (l[d] < 0) ? -1 : (l[d] >= G.nb[d]) ? 1 : 0;
+  if (o[0] == 0 && o[1] == 0 && o[2] == 0) return;
+  if (faces_only) {
+    int outside = (o[0] != 0) + (o[1] != 0) + (o[2] != 0);
+    bool deep = false;
+#pragma unroll
+    for (int d = 0; d < 3; d++) deep |= (l[d] < -2) || (l[d] >= G.nb[d] + 2);
+    if (outside > 1 || deep) return;
+  }
+  // read-only-path loads of the descriptor and the table entry (16 bytes each)
+  const longlong2 fd = __ldg(reinterpret_cast<const longlong2*>(sf) + slot);
+  const longlong2 raw =
+      __ldg(reinterpret_cast<const longlong2*>(fd.y) + ((o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)));
+  NbrEntry e;
+  e.src = reinterpret_cast<const double*>(raw.x);
+  e.mode = (int32_t)(raw.y & 0xffffffffll);
+  e.flip = (int32_t)((unsigned long long)raw.y >> 32);
+  SlotFill f;
+  f.dst = reinterpret_cast<double*>(fd.x);
+  if (e.src == nullptr) return;  // remote source: written by the halo exchange
+  int s[3];
+#pragma unroll
+  for (int d = 0; d < 3; d++) {
+    int m = (e.mode >> (2 * d)) & 3;
+    int n = G.nb[d];
+    if (o[d] == 0) s[d] = l[d];
+    else if (m == kShift) s[d] = l[d] - o[d] * n;
+    else if (m == kClamp) s[d] = (o[d] < 0) ? 0 : n - 1;
+    else s[d] = (o[d] < 0) ? -1 - l[d] : 2 * n - 1 - l[d];
+  }
+  long long so = cell_off(G, s[0], s[1], s[2]);
+  double* dst = f.dst + c;
+#pragma unroll
+  for (int v = 0; v < kNVar; v++) {
+    double x = e.src[v * G.cube + so];
+    if ((e.flip >> v) & 1) x = -x;
+    dst[v * G.cube] = x;
+  }
+}
+
+cudaError_t launch_fill_multi(const DevGrid& G, const SlotFill* sf, long long nslots, cudaStream_t s,
+                              int faces_only) {
+  const long long cells = (long long)G.P[0] * G.P[1] * G.P[2];
+  for (long long s0 = 0; s0 < nslots; s0 += 65535) {
+    const long long n = nslots - s0 < 65535 ? nslots - s0 : 65535;
+    fill_multi_kernel<<<dim3((unsigned)((cells + 255) / 256), (unsigned)n), 256, 0, s>>>(G, sf, s0, faces_only);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill(const DevGrid& G, double* state, int nslots, const NbrEntry* table,
                         cudaStream_t s, int faces_only) {
   long long total = (long long)nslots * G.P[0] * G.P[1] * G.P[2];
@@ -205,6 +272,38 @@ __global__ void __launch_bounds__(1024) dt_reduce_kernel(const DtRecord* __restr
 
 cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out, cudaStream_t s) {
   dt_reduce_kernel<<<1, 1024, 0, s>>>(records, n, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Several packets at once: the records of every packet (same rule, so the
+// result equals the host-side combination of the per-packet reductions) and
+// the packets' sticky status words (lowest first_bad, summed floor hits).
+__global__ void __launch_bounds__(1024) dt_reduce_multi_kernel(const PacketDt* __restrict__ pd, int npk,
+                                                               DtRecord* out, DevStatus* out_st) {
+  double s = -DBL_MAX;
+  long long g = LLONG_MAX;
+  for (int q = 0; q < npk; q++) {
+    const DtRecord* rec = pd[q].rec;
+    const long long n = pd[q].n;
+    for (long long t = threadIdx.x; t < n; t += blockDim.x) rec_combine(s, g, rec[t].s, rec[t].g);
+  }
+  block_reduce_rec<1024>(s, g);
+  if (threadIdx.x == 0) {
+    out->s = s;
+    out->g = g;
+    unsigned long long fb = ~0ull, fh = 0;
+    for (int q = 0; q < npk; q++) {
+      fb = pd[q].st->first_bad < fb ? pd[q].st->first_bad : fb;
+      fh += pd[q].st->floor_hits;
+    }
+    out_st->first_bad = fb;
+    out_st->floor_hits = fh;
+  }
+}
+
+cudaError_t launch_dt_reduce_multi(const PacketDt* pd, int npk, DtRecord* out, DevStatus* out_st, cudaStream_t s) {
+  dt_reduce_multi_kernel<<<1, 1024, 0, s>>>(pd, npk, out, out_st);
   count_launch();
   return cudaGetLastError();
 }

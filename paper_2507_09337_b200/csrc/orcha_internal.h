@@ -63,6 +63,20 @@ struct DtRecord {
   long long g;
 };
 
+// Multi-packet dt reduction: one packet's records and status word.
+struct PacketDt {
+  const DtRecord* rec;
+  long long n;
+  const DevStatus* st;
+};
+
+// Multi-packet guard fill: one slot's padded cube base and its 27 table entries.
+struct SlotFill {
+  double* dst;
+  const NbrEntry* tab;
+};
+static_assert(sizeof(SlotFill) == 16 && sizeof(NbrEntry) == 16, "16-byte descriptor loads (fill_multi_kernel)");
+
 struct SlotInfo {     // per slot: block coordinates (bi, bj, bk)
   int bc[3];
   int pad;
@@ -139,6 +153,9 @@ cudaError_t launch_status_reset(DevStatus* st, cudaStream_t s);
 cudaError_t launch_dt(const DevGrid& G, const double* state, int nslots, const SlotInfo* slots,
                       DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s);
 cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out, cudaStream_t s);
+cudaError_t launch_dt_reduce_multi(const PacketDt* pd, int npk, DtRecord* out, DevStatus* out_st, cudaStream_t s);
+cudaError_t launch_fill_multi(const DevGrid& G, const SlotFill* sf, long long nslots, cudaStream_t s,
+                              int faces_only);
 cudaError_t launch_advance(const DevGrid& G, double* state, double* u1, int nslots,
                            const SlotInfo* slots, const double* d_dt, double h_dt,
                            DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s);

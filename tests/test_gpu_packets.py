@@ -10,6 +10,8 @@ import pytest
 import orcha_inputs as inp
 from tests import gpu_helpers as H
 
+O, P, R = 0, 1, 2
+
 pytestmark = pytest.mark.gpu
 N = (64, 64, 64)
 STEPS = 4
@@ -56,3 +58,20 @@ def test_packet_sizes_bitwise_identical_production(oracle_ref, nb):
             continue
         G, _ = _run(nb, ps, False)
         assert np.array_equal(G, ref)
+
+
+def test_many_packets_one_launch_fill_and_dt():
+    # >= 128 packets: the fill runs as one launch over every slot of the set
+    # and dt as one reduction over every packet's records -- bitwise the same
+    # as one packet, and the launch count shows the batching
+    from paper_2507_09337_b200 import hydro
+    g = H.make_grid(3, (8, 8, 8), (8, 8, 4), bc=((R, O), (P, P), (O, R)))
+    U0 = inp.random_field(g.N, seed=44)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=3)
+    pk = H.gpu_setup(g, U0, npackets=128, shuffle=True)
+    n0 = g.lib.orcha_launch_count()
+    hydro.orcha_fill_guardcells(pk)
+    assert g.lib.orcha_launch_count() - n0 == 1
+    t, n, log = hydro.run(pk, nsteps=3)
+    assert [x[0] for x in log] == [x[0] for x in logA]
+    assert np.array_equal(H.gather(g, pk), A)

@@ -129,6 +129,27 @@ __host__ __device__ constexpr long long u1_cube() {
 // (push_cell), 2 into the x-guards only (push_cell_x, gather mode).
 // GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a
 // separate instantiation so the plain kernels carry none of its registers.
+// The x-axis part of push_cell (push.cuh) for a padded target (the states, or
+// the per-stage stage-1 buffers): interior cell (ci, cj, k) feeds the x-guards
+// of the blocks the two cached x entries name (gather fill mode).
+template <int NB>
+__device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, int ci, int cj, int k,
+                                       const double w[5]) {
+  const int side = ci >= NB - 4 ? 1 : (ci < 4 ? 0 : -1);
+  if (side < 0 || sxp[side].dst == nullptr) return;
+  const PushEntry e = sxp[side];
+  const int m = e.mode & 3;
+  int t0, cnt = 1;
+  if (m == kShift) t0 = side ? ci - NB : ci + NB;
+  else if (m == kMirror) t0 = side ? 2 * NB - 1 - ci : -1 - ci;
+  else { cnt = (side ? ci == NB - 1 : ci == 0) ? 4 : 0; t0 = side ? NB : -4; }
+  for (int xx = 0; xx < cnt; xx++) {
+    double* q = e.dst + cell_off(G, t0 + xx, cj, k);
+#pragma unroll
+    for (int v = 0; v < 5; v++) q[v * G.cube] = ((e.flip >> v) & 1) ? -w[v] : w[v];
+  }
+}
+
 // PLM + Riemann flux of one face.  SCH 0: the paper-path scheme (minmod +
 // HLL); SCH 1: the grid's F4 flags (limiter, Riemann solver) read at run time.
 template <int D, int SCH>
@@ -179,7 +200,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
   if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
   __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
-  if (STAGE == 1 && GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
+  if (GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     fence_mbar_init();
@@ -193,7 +214,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   auto issue = [&](int p) {
     if (p < Gm::NPLANES) {
       const int s = p % NS, lane = tid & 31;
-      if (STAGE == 1 && GATHER) {
+      if (GATHER) {
         // Gather mode: only the x-guards were filled.  Each staged row
         // (padded plane pp, padded row pr) is the (y, z) image of a row of
         // the block that owns it -- the neighbour table's (0, oy, oz) entry --
@@ -252,7 +273,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       bool fl;
       int r = c / IPX;
       double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
-      if (STAGE == 1 && GATHER) {  // gather mode: mirrored guard rows negate rho*v / rho*w
+      if (GATHER) {  // gather mode: mirrored guard rows negate rho*v / rho*w
         const unsigned fm = flipm[(p % NS) * Gm::IR + r];
         if (fm & 4) my = -my;
         if (fm & 8) mz = -mz;
@@ -346,7 +367,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
   if (tid < 32)
     for (int p = 0; p < NS; p++) issue(p);
-  if (STAGE == 1 && GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
+  if (GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
   for (int p = 0; p < 5; p++) {
     wait_plane(p);
     convert(p);
@@ -428,7 +449,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
           double w[5];
 #pragma unroll
           for (int v = 0; v < 5; v++) w[v] = un[v] - dt * D[v];
-          push_cell(G, push + slot * 27, ci, cj, k, w);
+          if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, w);
+          else push_x<NB>(G, sxp, ci, cj, k, w);  // gather mode: the x-guards only
         }
       } else {
         double nw[5];
@@ -438,22 +460,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 #pragma unroll
         for (int v = 0; v < 5; v++) dst[v * cube] = nw[v];
         if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
-        if (PUSH == 2) {  // x-guards only (the x-axis part of push_cell; both entries cached in shared memory)
-          const int side = ci >= NB - 4 ? 1 : (ci < 4 ? 0 : -1);
-          if (side >= 0 && sxp[side].dst != nullptr) {
-            const PushEntry e = sxp[side];
-            const int m = e.mode & 3;
-            int t0, cnt = 1;
-            if (m == kShift) t0 = side ? ci - NB : ci + NB;
-            else if (m == kMirror) t0 = side ? 2 * NB - 1 - ci : -1 - ci;
-            else { cnt = (side ? ci == NB - 1 : ci == 0) ? 4 : 0; t0 = side ? NB : -4; }
-            for (int xx = 0; xx < cnt; xx++) {
-              double* q = e.dst + cell_off(G, t0 + xx, cj, k);
-#pragma unroll
-              for (int v = 0; v < 5; v++) q[v * cube] = ((e.flip >> v) & 1) ? -nw[v] : nw[v];
-            }
-          }
-        }
+        if (PUSH == 2) push_x<NB>(G, sxp, ci, cj, k, nw);  // next step's x-guards
         bool f2;
         Prim q = eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
         double s = signal_speed<3>(q, G);
@@ -477,6 +484,12 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
                              const PushEntry* push = nullptr, const NbrEntry* nbr = nullptr,
                              int pushkind = 1) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
+  // Instantiations: PUSH 0 / 1 / 2 x plain, PUSH 0 / 2 x gather (stage 1:
+  // from the states; per-stage stage 2: from the stage-1 buffers).  PUSH 2
+  // (x-guards only) exists for the kernels that feed a gather-mode step:
+  // telescoped stage 2 and both per-stage stages.
+  constexpr bool P2 = (STAGE == 2) || (MODE == 1);
+  constexpr bool GA = (STAGE == 1) || (MODE == 1);
   static bool attr = false;
   if (!attr) {
     const int sm = (int)Gm::SMEM;
@@ -484,32 +497,41 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false, SCH>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (STAGE == 1)
+    if constexpr (GA)
       cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true, SCH>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (STAGE == 2 && MODE == 0)
+    if constexpr (P2)
       cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false, SCH>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if constexpr (P2 && GA)
+      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, true, SCH>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     attr = true;
   }
   // the guard-push epilogues and the gather staging are separate
   // instantiations so the default kernels carry none of their registers
   const dim3 grid(nslots * SPLIT);
+#define ORCHA_K(P, GT)                                                                                  \
+  stage_fused_kernel<NB, STAGE, SPLIT, MODE, P, GT, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, \
+                                                                                      d_dt, h_dt, records, st, \
+                                                                                      push, nbr)
   if (push && pushkind == 2) {
-    if constexpr (STAGE == 2 && MODE == 0)
-      stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr);
+    if constexpr (P2) {
+      if constexpr (GA) {
+        if (nbr) ORCHA_K(2, true);
+        else ORCHA_K(2, false);
+      } else {
+        ORCHA_K(2, false);
+      }
+    }
   } else if (push) {
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr);
+    ORCHA_K(1, false);
   } else if (nbr) {
-    if constexpr (STAGE == 1)
-      stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nbr);
+    if constexpr (GA) ORCHA_K(0, true);
   } else {
-    stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nullptr);
+    ORCHA_K(0, false);
   }
+#undef ORCHA_K
   count_launch();
 }
 
@@ -553,12 +575,12 @@ template <int NB, int SCH>
 static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                    const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                                    long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
-                                   const NbrEntry* nbr) {
+                                   const NbrEntry* nbr, int pk) {
   constexpr int SP = (NB == 16) ? 2 : (NB == 32) ? 4 : 1;
   if (stage == 1) {
-    launch_stage<NB, 1, SP, 1, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nbr);
+    launch_stage<NB, 1, SP, 1, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nbr, pk);
   } else {
-    launch_stage<NB, 2, SP, 1, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push);
+    launch_stage<NB, 2, SP, 1, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nbr, pk);
     *nrecords = (long long)nslots * SP;
   }
   return cudaGetLastError();
@@ -575,9 +597,9 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
   cudaError_t fused_stage_n##NB##_s##SCH(const DevGrid& G, int stage, double* state, double* u1, int nslots,    \
                                          const SlotInfo* slots, const double* d_dt, double h_dt,                \
                                          DtRecord* records, long long* nrecords, DevStatus* st,                 \
-                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr) {          \
+                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk) {  \
     return launch_stage_nb<NB, SCH>(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s,   \
-                                    push, nbr);                                                                  \
+                                    push, nbr, pk);                                                              \
   }
 
 }  // namespace orcha

@@ -12,7 +12,7 @@ namespace orcha {
   cudaError_t fused_stage_n##NB##_s##SCH(const DevGrid& G, int stage, double* state, double* u1, int nslots,    \
                                          const SlotInfo* slots, const double* d_dt, double h_dt,                \
                                          DtRecord* records, long long* nrecords, DevStatus* st,                 \
-                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr);
+                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk);
 ORCHA_FUSED_DECL(8, 0)
 ORCHA_FUSED_DECL(8, 1)
 ORCHA_FUSED_DECL(16, 0)
@@ -62,17 +62,19 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
 // One stage of the per-stage variant (F1): stage 1 -> U1 (padded, interior
 // only), stage 2 -> U^{n+1} in place + dt records.  `push` (optional): the
 // push tables of the buffer this stage writes (stage 1: the stage-1 buffers,
-// stage 2: the states); `nbr` (optional, stage 1, gather mode) as above.
+// stage 2: the states; with push_x_only the x-guards only); `nbr` (optional,
+// gather mode): stage 1 the states' neighbour tables, stage 2 the stage-1
+// buffers'.
 cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                                long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
-                               const NbrEntry* nbr) {
+                               const NbrEntry* nbr, bool push_x_only) {
   if (!fused_supported(G))
     return launch_stage_ref(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  const NbrEntry* n1 = (stage == 1) ? nbr : nullptr;
+  const int pk = push_x_only ? 2 : 1;
   const bool var = G.riemann != 0 || G.limiter != 0;
 #define ORCHA_STG(NB, SCH) \
-  fused_stage_n##NB##_s##SCH(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, n1)
+  fused_stage_n##NB##_s##SCH(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk)
   if (G.nb[0] == 16) return var ? ORCHA_STG(16, 1) : ORCHA_STG(16, 0);
   if (G.nb[0] == 32) return var ? ORCHA_STG(32, 1) : ORCHA_STG(32, 0);
   return var ? ORCHA_STG(8, 1) : ORCHA_STG(8, 0);

@@ -127,6 +127,12 @@ struct orcha_packet {
   // the y/z guard rows from the owning blocks through d_nbr
   bool guards_xonly;
   const orcha::NbrEntry* d_nbr;
+  // per-stage variant, gather mode: stage 1 scattered U1 into the U1
+  // x-guards; the stage-1 buffer "fill" then only marks them valid and stage
+  // 2 stages its y/z guard rows of U1 from the owning blocks (d_nbr_u1)
+  bool u1_xpushed;
+  bool u1_guards_xonly;
+  const orcha::NbrEntry* d_nbr_u1;
 };
 
 namespace orcha {

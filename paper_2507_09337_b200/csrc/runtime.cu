@@ -64,7 +64,7 @@ cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double*
 cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                                const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                                long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
-                               const NbrEntry* nbr);
+                               const NbrEntry* nbr, bool push_x_only);
 bool fused_supported(const DevGrid& G);
 }  // namespace orcha
 
@@ -328,6 +328,8 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
   p->xguards_pushed = false;
   p->guards_xonly = false;
   p->d_nbr = nullptr;
+  p->u1_xpushed = p->u1_guards_xonly = false;
+  p->d_nbr_u1 = nullptr;
   std::vector<SlotInfo> si(n);
   const DevGrid& G = g->dev;
   for (int s = 0; s < n; s++) {
@@ -388,6 +390,7 @@ static int32_t pack_impl(orcha_packet* p, const double* src, cudaMemcpyKind kind
   p->u1_guards_valid = false;
   p->guards_pushed = p->u1_pushed = false;  // new interior, not scattered into any guards
   p->xguards_pushed = false;
+  p->u1_xpushed = p->u1_guards_xonly = false;
   return ORCHA_OK;
 }
 
@@ -715,6 +718,20 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   const DevGrid& G0 = pk[0]->grid->dev;
   const bool xonly = buffer == 0 && npk == 1 && !push_enabled() && fill_mode() == 1 &&
                      kernel_variant() == 1 && fused_supported(G0);
+  // per-stage stage-1 buffer in gather mode: stage 1 wrote the U1 x-guards
+  // (same plan), stage 2 stages the y/z rows of U1 from their owners
+  const bool xonly_u1 = buffer == 1 && npk == 1 && !push_enabled() && fill_mode() == 1 && kernel_variant() == 1 &&
+                        fused_supported(G0) && pk[0]->u1_xpushed && pk[0]->push_plan == f;
+  if (xonly_u1) {
+    if (f->edge_fix[0]) {  // exchanged rows' resident-sourced x-guard parts
+      cudaError_t e = launch_fill(G0, pk[0]->scratch, pk[0]->nslots, f->d_tables_u1[0], s, 2);
+      if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
+    }
+    pk[0]->u1_guards_valid = true;
+    pk[0]->u1_guards_xonly = true;
+    pk[0]->d_nbr_u1 = f->d_tables_u1[0];
+    return ORCHA_OK;
+  }
   // several packets, full tables: every slot of the set in one launch
   // (from 128 packets on: the one-launch kernel pays a dependent descriptor
   // load per cell, ~0.5 ms on 16.8 M cells, which below that is more than the
@@ -751,6 +768,7 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
     pk[q]->push_plan = f;
     if (buffer) {
       pk[q]->u1_guards_valid = true;
+      pk[q]->u1_guards_xonly = false;
     } else {
       pk[q]->guards_valid = true;
       pk[q]->guards_xonly = xonly;
@@ -871,6 +889,7 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   p->stage1_done = false;
   p->u1_guards_valid = false;
   p->u1_pushed = false;
+  p->u1_xpushed = p->u1_guards_xonly = false;  // the scratch now holds the telescoped U1
   return ORCHA_OK;
 }
 
@@ -896,27 +915,39 @@ static int32_t stage_impl(orcha_packet* p, int32_t stage, const double* d_dt, do
   const bool fused = kernel_variant() == 1;
   if (stage == 1 && p->guards_xonly && !fused)
     return fail(ORCHA_E_STATE, "the gather-mode fill was done for the fused kernels; refill after changing the variant");
+  if (stage == 2 && p->u1_guards_xonly && !fused)
+    return fail(ORCHA_E_STATE, "the gather-mode refill was done for the fused kernels; refill after changing the variant");
   const PushEntry* push = nullptr;
   if (fused && push_enabled() && fused_supported(G) && p->push_plan) push = (stage == 1) ? p->d_push_u1 : p->d_push;
+  // gather mode: each stage also writes the x-guards the next gather-mode
+  // step reads (stage 1: U1's, stage 2: the state's), so no fill kernel runs
+  const bool xpush = fused && !push && p->guards_xonly && p->push_plan != nullptr && fused_supported(G);
+  if (xpush) push = (stage == 1) ? p->d_push_u1 : p->d_push;
+  const NbrEntry* nbr = (stage == 1) ? (p->guards_xonly ? p->d_nbr : nullptr)
+                                     : (p->u1_guards_xonly ? p->d_nbr_u1 : nullptr);
   if (!fused)
     e = launch_stage_ref(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                          &p->nrecords, p->status, s);
   else
     e = launch_stage_fused(G, stage, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                           &p->nrecords, p->status, s, push, (stage == 1 && p->guards_xonly) ? p->d_nbr : nullptr);
+                           &p->nrecords, p->status, s, push, nbr, xpush);
   if (e != cudaSuccess) return cuda_fail(e, "stage kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   if (stage == 1) {
     p->stage1_done = true;
     p->u1_guards_valid = false;
-    p->u1_pushed = push != nullptr;
+    p->u1_guards_xonly = false;
+    p->u1_pushed = push != nullptr && !xpush;
+    p->u1_xpushed = xpush;
   } else {
     p->stage1_done = false;
     p->u1_guards_valid = false;
+    p->u1_guards_xonly = false;
     p->u1_pushed = false;
+    p->u1_xpushed = false;
     p->guards_valid = false;
-    p->guards_pushed = push != nullptr;
-    p->xguards_pushed = false;
+    p->guards_pushed = push != nullptr && !xpush;
+    p->xguards_pushed = xpush;
     p->records_valid = true;
   }
   return ORCHA_OK;

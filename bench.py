@@ -320,7 +320,8 @@ def main():
         # SURVEY 8(f) F1, measured beside the paper's telescoped step (same protocol)
         variants["per-stage"] = timed_variant("per-stage", args.steps)
         variants["per-stage"]["note"] = ("fill -> dt -> stage 1 (interior) -> U1 guard refill -> stage 2; "
-                                         "oracle mode 'refill'")
+                                         "oracle mode 'refill'; gather fill mode: no fill kernel runs (stage 1 "
+                                         "writes the U1 x-guards, stage 2 stages U1 guard rows from their owners)")
         # restore the packet to a telescoped-step history is not needed: both
         # variants advance the same Sedov state, timing only
 

@@ -5,6 +5,8 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import shutil
+import tempfile
 import os
 import subprocess
 import sys
@@ -62,8 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> list:
     """Compile every translation unit of both libraries (production and
     parity) in one pool, then link each library."""
     out = []
-    objdir = os.path.join(HERE, "build")
-    os.makedirs(objdir, exist_ok=True)
+    objdir = tempfile.mkdtemp(prefix="orcha_build_")  # objects are not kept: every stale library is relinked whole
     todo = {}
     for lib, flags in VARIANTS.items():
         target = os.path.join(HERE, lib)
@@ -87,6 +88,7 @@ def build(force: bool = False, verbose: bool = False) -> list:
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         os.replace(tmp, target)
+    shutil.rmtree(objdir, ignore_errors=True)
     return out
 
 

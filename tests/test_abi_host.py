@@ -115,3 +115,40 @@ def test_advance_requires_fill_is_documented():
     # precede it) is stated in the header next to the entry point
     src = open(HEADER).read()
     assert "ORCHA_E_STATE" in src and "P:L674" in src
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    # the binding's struct layouts equal the C compiler's for include/orcha.h
+    # (sizes and every field offset), so the marshalling cannot drift
+    fields = {"orcha_grid_desc": abi.orcha_grid_desc, "orcha_dt_info": abi.orcha_dt_info}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "orcha.h"', "int main(void) {"]
+    for name, cls in fields.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = dict(line.rsplit(" ", 1) for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                              check=True).stdout.split("\n") if line)
+    for name, cls in fields.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
+
+
+def test_scheme_flags_validated(lib):
+    d = desc()
+    d.riemann = 2
+    assert create(lib, d)[0] == -1
+    d = desc()
+    d.limiter = -1
+    assert create(lib, d)[0] == -1
+    d = desc()
+    d.riemann, d.limiter = abi.RIEMANN_HLLC, abi.LIMITER_MC
+    rc, h = create(lib, d)
+    assert rc == 0
+    lib.orcha_grid_destroy(h)

@@ -154,6 +154,17 @@ int32_t orcha_packet_unpack(const orcha_packet* packet, double* h_interior, void
 int32_t orcha_packet_pack_device(orcha_packet* packet, const double* d_interior, void* stream);
 int32_t orcha_packet_unpack_device(const orcha_packet* packet, double* d_interior, void* stream);
 
+/* Unpack without the synchronizing status check, for streamed packets
+ * (packets shipped in and out every cycle on copy streams
+ * overlapping the other packets' compute): the gather kernel and
+ * the copy into `interior` (pinned host or device memory; any address the
+ * runtime can copy to asynchronously) are only enqueued on `stream`.  The
+ * packet's sticky status is reported by the next orcha_compute_dt or
+ * synchronizing unpack.  The packet's scratch holds the staged data until
+ * the copy has run: order the next pack / advance of this packet after it.
+ * Errors: ORCHA_E_ARG, ORCHA_E_CUDA. */
+int32_t orcha_packet_unpack_async(const orcha_packet* packet, double* interior, void* stream);
+
 /* -------------------------------------------------------- the hot path -- */
 
 /* Guard-cell fill ("We assume that the first refresh occurs before we invoke

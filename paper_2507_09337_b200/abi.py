@@ -29,6 +29,7 @@ EXPORTS = [
     "orcha_comm_create", "orcha_comm_destroy", "orcha_set_kernel_variant", "orcha_get_kernel_variant",
     "orcha_comm_create_local", "orcha_comm_push", "orcha_comm_plan", "orcha_hydro_stage",
     "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push", "orcha_set_fill_mode",
+    "orcha_packet_unpack_async",
 ]
 
 
@@ -86,6 +87,7 @@ _SIGS = {
     "orcha_packet_unpack": (_i32, [_vp, _vp, _vp]),
     "orcha_packet_pack_device": (_i32, [_vp, _vp, _vp]),
     "orcha_packet_unpack_device": (_i32, [_vp, _vp, _vp]),
+    "orcha_packet_unpack_async": (_i32, [_vp, _vp, _vp]),
     "orcha_fill_guardcells": (_i32, [_P(_vp), _i32, _vp, _vp]),
     "orcha_compute_dt": (_i32, [_P(_vp), _i32, _vp, _dbl, _P(orcha_dt_info), _vp]),
     "orcha_hydro_advance": (_i32, [_vp, _dbl, _vp]),

@@ -428,6 +428,15 @@ extern "C" int32_t orcha_packet_pack_device(orcha_packet* p, const double* d, vo
 extern "C" int32_t orcha_packet_unpack(const orcha_packet* p, double* h, void* stream) {
   return unpack_impl(p, h, cudaMemcpyDeviceToHost, stream);
 }
+extern "C" int32_t orcha_packet_unpack_async(const orcha_packet* p, double* dst, void* stream) {
+  if (!p || !dst) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = launch_pack(p->grid->dev, p->state, p->scratch, p->nslots, false, s);
+  if (e != cudaSuccess) return cuda_fail(e, "unpack kernel");
+  e = cudaMemcpyAsync(dst, p->scratch, interior_bytes(p), cudaMemcpyDefault, s);
+  if (e != cudaSuccess) return cuda_fail(e, "unpack copy");
+  return ORCHA_OK;
+}
 extern "C" int32_t orcha_packet_unpack_device(const orcha_packet* p, double* d, void* stream) {
   return unpack_impl(p, d, cudaMemcpyDeviceToDevice, stream);
 }

@@ -112,7 +112,15 @@ class Packet:
         name = "orcha_packet_pack_device" if t.is_cuda else "orcha_packet_pack"
         abi.call(self.lib, name, self.handle, ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(_stream_ptr(stream)))
 
-    def unpack(self, out=None, stream=None) -> np.ndarray:
+    def unpack(self, out=None, stream=None, sync: bool = True) -> np.ndarray:
+        """Interior data of the packet's blocks.  sync=False (torch pinned-host
+        or device `out` only): orcha_packet_unpack_async, enqueued on `stream`
+        without the status check."""
+        if not sync:
+            assert isinstance(out, torch.Tensor) and (out.is_cuda or out.is_pinned())
+            abi.call(self.lib, "orcha_packet_unpack_async", self.handle, ctypes.c_void_p(out.data_ptr()),
+                     ctypes.c_void_p(_stream_ptr(stream)))
+            return out
         if out is None:
             out = np.empty(self.interior_shape, dtype=np.float64)
         if isinstance(out, np.ndarray):

@@ -75,3 +75,51 @@ def test_many_packets_one_launch_fill_and_dt():
     t, n, log = hydro.run(pk, nsteps=3)
     assert [x[0] for x in log] == [x[0] for x in logA]
     assert np.array_equal(H.gather(g, pk), A)
+
+
+def test_streamed_host_mesh_equals_resident_run():
+    # SURVEY 8(f) F3 / bench.py's e2e: the mesh lives in pinned host memory as
+    # K packets shipped in (H2D stream), advanced, and shipped out with
+    # orcha_packet_unpack_async (D2H stream) every step, the next step reading
+    # the host mesh -- bitwise the device-resident run
+    import math
+    import torch
+    from paper_2507_09337_b200 import hydro
+    g = H.make_grid(3, (8, 8, 8), (4, 4, 4), bc=((R, O), (P, P), (O, R)))
+    U0 = inp.random_field(g.N, seed=51)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
+    slabs = [a for a in np.array_split(np.arange(g.nblocks), 4)]
+    pks = [hydro.Packet(g, a) for a in slabs]
+    mesh = [torch.from_numpy(inp.to_blocks(U0, g.nb, a)).pin_memory() for a in slabs]
+    comp, h2d, d2h = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    done = [None] * len(pks)
+    dts = []
+    for _ in range(4):
+        ev = []
+        for i, p in enumerate(pks):
+            if done[i] is not None:
+                h2d.wait_event(done[i])
+            p.pack(mesh[i], h2d)
+            e = torch.cuda.Event()
+            e.record(h2d)
+            ev.append(e)
+        for e in ev:
+            comp.wait_event(e)
+        hydro.orcha_fill_guardcells(pks, None, comp)
+        info = hydro.orcha_compute_dt(pks, math.inf, None, comp)
+        dts.append(info.dt)
+        for i, p in enumerate(pks):
+            hydro.orcha_hydro_advance(p, info.dt, comp)
+            e = torch.cuda.Event()
+            e.record(comp)
+            d2h.wait_event(e)
+            p.unpack(mesh[i], d2h, sync=False)
+            e2 = torch.cuda.Event()
+            e2.record(d2h)
+            done[i] = e2
+    torch.cuda.synchronize()
+    out = None
+    for a, m in zip(slabs, mesh):
+        out = inp.from_blocks(m.numpy(), g.N, g.nb, a, out)
+    assert dts == [x[0] for x in logA]
+    assert np.array_equal(out, A)

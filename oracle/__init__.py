@@ -40,6 +40,7 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-st
 OUTFLOW, PERIODIC, REFLECT = 0, 1, 2
 HLL, HLLC = 0, 1          # Riemann solver flag
 MINMOD, MC = 0, 1         # limiter flag
+GAMMA_LAW, GAS_RADIATION = 0, 1   # EOS flag (SURVEY 8(f) F4 expensive-EOS surrogate)
 TAG_CFL, TAG_CLAMP = 0, 1
 
 
@@ -65,6 +66,9 @@ class _CGrid(ctypes.Structure):
         ("smallp", ctypes.c_double),
         ("riemann", ctypes.c_int32),
         ("limiter", ctypes.c_int32),
+        ("eos", ctypes.c_int32),
+        ("eos_work", ctypes.c_int32),
+        ("arad", ctypes.c_double),
     ]
 
 
@@ -95,6 +99,8 @@ def _load():
         lib.oracle_hllc.restype = None
         lib.oracle_mc_slope.argtypes = [d, d, d]
         lib.oracle_mc_slope.restype = d
+        lib.oracle_eint_from_p.argtypes = [g, d, d]
+        lib.oracle_eint_from_p.restype = d
         lib.oracle_face_flux.argtypes = [g, ctypes.c_int, dp, dp, dp, dp, dp]
         lib.oracle_face_flux.restype = None
         lib.oracle_dt.argtypes = [g, dp, d, dp, P(ctypes.c_int64), P(ctypes.c_int32), dp]
@@ -119,6 +125,9 @@ class Grid:
     smallp: float = 1e-30
     riemann: int = HLL                      # F4: HLL (default) or HLLC
     limiter: int = MINMOD                   # F4: minmod (default) or MC
+    eos: int = GAMMA_LAW                    # F4: gamma law (default) or gas + radiation (Newton)
+    eos_work: int = 1                       # F4: temperature solves per EOS evaluation
+    arad: float = 0.0                       # F4: radiation constant a
 
     @property
     def ndim(self) -> int:
@@ -155,6 +164,9 @@ class Grid:
         cg.smallp = self.smallp
         cg.riemann = int(self.riemann)
         cg.limiter = int(self.limiter)
+        cg.eos = int(self.eos)
+        cg.eos_work = int(self.eos_work)
+        cg.arad = float(self.arad)
         return cg
 
 
@@ -191,6 +203,10 @@ def sound_speed(grid: Grid, q5: Sequence[float]) -> float:
 
 def minmod_slope(qm: float, q0: float, qp: float) -> float:
     return _load().oracle_minmod_slope(qm, q0, qp)
+
+
+def eint_from_p(grid: Grid, rho: float, p: float) -> float:
+    return _load().oracle_eint_from_p(ctypes.byref(grid.c()), rho, p)
 
 
 def mc_slope(qm: float, q0: float, qp: float) -> float:

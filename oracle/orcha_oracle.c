@@ -35,7 +35,11 @@
  *     0 (reading c21);
  *   - Riemann solver HLLC (Toro, "Riemann Solvers and Numerical Methods for
  *     Fluid Dynamics", 3rd ed., sec 10.4, eqs 10.37-10.39), same wave speeds
- *     as HLL (reading c20).
+ *     as HLL (reading c20);
+ *   - expensive-EOS surrogate (reading c22; the paper's Helmholtz EOS makes the
+ *     GPU favourable): ideal gas + radiation with c_v = 1,
+ *     rho e = rho T + a T^4, p = (gamma-1) rho T + a T^4 / 3, temperature by
+ *     Newton iteration, sound speed from Chandrasekhar's Gamma_1.
  * The "refill" mode (ghosts of U1 refilled between the stages) is the plain
  * two-refresh scheme that P:L667-668 describes before the trick; it is the
  * oracle of SURVEY 8(f) F1 and the telescoping equivalence pin.
@@ -54,6 +58,9 @@ typedef struct {
   double gamma, cfl, smallp;
   int32_t riemann;    /* 0 HLL, 1 HLLC (F4) */
   int32_t limiter;    /* 0 minmod, 1 MC (F4) */
+  int32_t eos;        /* 0 gamma law, 1 gas + radiation by Newton (F4 expensive-EOS surrogate) */
+  int32_t eos_work;   /* eos 1: temperature solves per evaluation (>= 1; the surrogate's cost knob) */
+  double arad;        /* eos 1: radiation constant a (code units) */
 } oracle_grid;
 
 enum { BC_OUTFLOW = 0, BC_PERIODIC = 1, BC_REFLECT = 2 };
@@ -79,6 +86,7 @@ static int check_grid(const oracle_grid* G) {
   if (G->ndim < 1 || G->ndim > 3) return ORC_E_ARG;
   if (G->ng < 4) return ORC_E_ARG;
   if (G->riemann < 0 || G->riemann > 1 || G->limiter < 0 || G->limiter > 1) return ORC_E_ARG;
+  if (G->eos < 0 || G->eos > 1 || (G->eos == 1 && (G->eos_work < 1 || !(G->arad >= 0.0)))) return ORC_E_ARG;
   for (int d = 0; d < 3; d++) {
     if (d < G->ndim) {
       if (G->N[d] < G->ng) return ORC_E_ARG;
@@ -139,6 +147,53 @@ int oracle_fill_ghosts(const oracle_grid* G, double* U) {
 
 /* ------------------------------------------------- 2. EOS */
 
+/* Expensive-EOS surrogate (reading c22).  Newton for T from the gas-only
+ * guess, stopping when |dT| <= 1e-14 |T| or after 50 iterations; the solve is
+ * repeated eos_work times, each repeat restarting from the guess (`+ 0.0 *
+ * T` keeps the repeats data-dependent without changing a finite guess), so the
+ * result is that of one solve. */
+static double temp_from_e(const oracle_grid* G, double rho, double eint) {
+  double T = 0.0;
+  for (int r = 0; r < G->eos_work; r++) {
+    T = eint + 0.0 * T;
+    for (int it = 0; it < 50; it++) {
+      double T3 = (T * T) * T;
+      double f = (T + (G->arad * (T3 * T)) / rho) - eint;
+      double fp = 1.0 + ((4.0 * G->arad) * T3) / rho;
+      double dT = f / fp;
+      T = T - dT;
+      if (fabs(dT) <= 1e-14 * fabs(T)) break;
+    }
+  }
+  return T;
+}
+
+static double temp_from_p(const oracle_grid* G, double rho, double p) {
+  double gr = (G->gamma - 1.0) * rho;
+  double T = 0.0;
+  for (int r = 0; r < G->eos_work; r++) {
+    T = p / gr + 0.0 * T;
+    for (int it = 0; it < 50; it++) {
+      double T3 = (T * T) * T;
+      double f = (gr * T + (G->arad * (T3 * T)) / 3.0) - p;
+      double fp = gr + ((4.0 * G->arad) * T3) / 3.0;
+      double dT = f / fp;
+      T = T - dT;
+      if (fabs(dT) <= 1e-14 * fabs(T)) break;
+    }
+  }
+  return T;
+}
+
+/* Gamma_1 of the gas + radiation mixture (Chandrasekhar), beta = p_gas / p:
+ *   Gamma_1 = beta + (4 - 3 beta)^2 (gamma - 1) / (beta + 12 (gamma - 1)(1 - beta)) */
+static double gamma1(const oracle_grid* G, double rho, double p, double T) {
+  double g1 = G->gamma - 1.0;
+  double beta = (g1 * rho * T) / p;
+  double x = 4.0 - 3.0 * beta;
+  return beta + ((x * x) * g1) / (beta + (12.0 * g1) * (1.0 - beta));
+}
+
 /* Primitive recovery; returns 1 if the floor fired, -1 if !(rho > 0). */
 int oracle_prim(const oracle_grid* G, const double U[5], double q[5]) {
   double rho = U[0];
@@ -147,7 +202,13 @@ int oracle_prim(const oracle_grid* G, const double U[5], double q[5]) {
   double v = U[2] * ir;
   double w = U[3] * ir;
   double ke = (0.5 * rho) * ((u * u + v * v) + w * w);
-  double p = (G->gamma - 1.0) * (U[4] - ke);
+  double p;
+  if (G->eos == 0) {
+    p = (G->gamma - 1.0) * (U[4] - ke);
+  } else {
+    double T = temp_from_e(G, rho, (U[4] - ke) * ir);
+    p = ((G->gamma - 1.0) * rho) * T + (G->arad * ((T * T) * (T * T))) / 3.0;
+  }
   int hit = 0;
   if (p < G->smallp) { p = G->smallp; hit = 1; } /* NaN is kept (c10) */
   q[0] = rho; q[1] = u; q[2] = v; q[3] = w; q[4] = p;
@@ -156,7 +217,15 @@ int oracle_prim(const oracle_grid* G, const double U[5], double q[5]) {
 }
 
 double oracle_sound_speed(const oracle_grid* G, const double q[5]) {
-  return sqrt((G->gamma * q[4]) / q[0]);
+  if (G->eos == 0) return sqrt((G->gamma * q[4]) / q[0]);
+  double T = temp_from_p(G, q[0], q[4]);
+  return sqrt((gamma1(G, q[0], q[4], T) * q[4]) / q[0]);
+}
+
+/* Specific internal energy of (rho, p) under the expensive EOS (tests). */
+double oracle_eint_from_p(const oracle_grid* G, double rho, double p) {
+  double T = temp_from_p(G, rho, p);
+  return T + (G->arad * ((T * T) * (T * T))) / rho;
 }
 
 /* ---------------------------------------- 3. PLM/minmod */
@@ -191,8 +260,15 @@ static void cons_and_flux(const oracle_grid* G, int d, const double q[5], double
                           double* c) {
   double gam = G->gamma;
   double ig1 = 1.0 / (gam - 1.0);
-  *c = sqrt((gam * q[4]) / q[0]);
-  double E = q[4] * ig1 + (0.5 * q[0]) * ((q[1] * q[1] + q[2] * q[2]) + q[3] * q[3]);
+  double E;
+  if (G->eos == 0) {
+    *c = sqrt((gam * q[4]) / q[0]);
+    E = q[4] * ig1 + (0.5 * q[0]) * ((q[1] * q[1] + q[2] * q[2]) + q[3] * q[3]);
+  } else {
+    double T = temp_from_p(G, q[0], q[4]);
+    *c = sqrt((gamma1(G, q[0], q[4], T) * q[4]) / q[0]);
+    E = (q[0] * T + G->arad * ((T * T) * (T * T))) + (0.5 * q[0]) * ((q[1] * q[1] + q[2] * q[2]) + q[3] * q[3]);
+  }
   U[0] = q[0];
   U[1] = q[0] * q[1];
   U[2] = q[0] * q[2];

@@ -80,10 +80,19 @@ typedef struct {
    * (A6) or ORCHA_LIMITER_MC (monotonized central, reading c21). */
   int32_t riemann;
   int32_t limiter;
+  /* F4 expensive-EOS surrogate (reading c22): eos = ORCHA_EOS_GAMMA_LAW (A5)
+   * or ORCHA_EOS_GAS_RADIATION: ideal gas + radiation with c_v = 1,
+   * rho e = rho T + arad T^4, p = (gamma-1) rho T + arad T^4 / 3, the
+   * temperature by Newton iteration (repeated eos_work >= 1 times: the
+   * surrogate's cost knob), sound speed from Chandrasekhar's Gamma_1. */
+  int32_t eos;
+  int32_t eos_work;
+  double arad;
 } orcha_grid_desc;
 
 enum { ORCHA_RIEMANN_HLL = 0, ORCHA_RIEMANN_HLLC = 1 };
 enum { ORCHA_LIMITER_MINMOD = 0, ORCHA_LIMITER_MC = 1 };
+enum { ORCHA_EOS_GAMMA_LAW = 0, ORCHA_EOS_GAS_RADIATION = 1 };
 
 typedef struct orcha_grid orcha_grid;
 typedef struct orcha_packet orcha_packet;
@@ -102,7 +111,8 @@ typedef struct {
 
 /* Validate `desc` and create a grid handle (host only, no device work).
  * Errors: ORCHA_E_ARG (ndim, nb, nblk, extents, bc codes, gamma <= 1,
- * cfl <= 0, riemann / limiter codes), ORCHA_E_HALO (ng < 4), ORCHA_E_ARG if a periodic axis has fewer
+ * cfl <= 0, riemann / limiter / eos codes, eos_work < 1 or arad < 0 with the
+ * gas + radiation EOS), ORCHA_E_HALO (ng < 4), ORCHA_E_ARG if a periodic axis has fewer
  * cells than ng. */
 int32_t orcha_grid_create(const orcha_grid_desc* desc, orcha_grid** out);
 int32_t orcha_grid_destroy(orcha_grid* grid);

@@ -18,6 +18,7 @@ STATUS = {0: "ORCHA_OK", -1: "ORCHA_E_ARG", -2: "ORCHA_E_RANGE", -3: "ORCHA_E_HA
 BC_OUTFLOW, BC_PERIODIC, BC_REFLECT = 0, 1, 2
 RIEMANN_HLL, RIEMANN_HLLC = 0, 1
 LIMITER_MINMOD, LIMITER_MC = 0, 1
+EOS_GAMMA_LAW, EOS_GAS_RADIATION = 0, 1
 DT_CFL, DT_CLAMP = 0, 1
 
 EXPORTS = [
@@ -54,6 +55,9 @@ class orcha_grid_desc(ctypes.Structure):
         ("smallp", ctypes.c_double),
         ("riemann", ctypes.c_int32),
         ("limiter", ctypes.c_int32),
+        ("eos", ctypes.c_int32),
+        ("eos_work", ctypes.c_int32),
+        ("arad", ctypes.c_double),
     ]
 
 

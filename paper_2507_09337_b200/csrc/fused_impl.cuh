@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         if (fm & 4) my = -my;
         if (fm & 8) mz = -mz;
       }
-      Prim q = eos(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl);
+      Prim q = (SCH == 0) ? eos(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl)
+                          : eos_var(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl);
       int x = c - r * IPX - INO, y = jj0 + ORG + r - INO;
       // own (non-overlapping) rows of the band only, so each cell counts once
       bool mine = r >= 2 && r < 2 + H;
@@ -462,8 +463,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
         if (PUSH == 2) push_x<NB>(G, sxp, ci, cj, k, nw);  // next step's x-guards
         bool f2;
-        Prim q = eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
-        double s = signal_speed<3>(q, G);
+        Prim q = (SCH == 0) ? eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2)
+                            : eos_var(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
+        double s = (SCH == 0) ? signal_speed<3>(q, G) : signal_speed_var<3>(q, G);
         long long g = (((long long)si.bc[2] * NB + k) * G.N[1] + ((long long)si.bc[1] * NB + cj)) * G.N[0] +
                       ((long long)si.bc[0] * NB + ci);
         if (dt_better(s, g, s_rec, g_rec)) { s_rec = s; g_rec = g; }

@@ -236,8 +236,8 @@ __global__ void __launch_bounds__(256) dt_kernel(DevGrid G, const double* __rest
     int k = (int)(c / ((long long)G.nb[0] * G.nb[1]));
     const double* p = state + slot * kNVar * G.cube + cell_off(G, i, j, k);
     bool fl;
-    Prim q = eos(p[0], p[G.cube], p[2 * G.cube], p[3 * G.cube], p[4 * G.cube], G, &fl);
-    s = signal_speed<NDIM>(q, G);
+    Prim q = eos_var(p[0], p[G.cube], p[2 * G.cube], p[3 * G.cube], p[4 * G.cube], G, &fl);
+    s = signal_speed_var<NDIM>(q, G);
     SlotInfo si = slots[slot];
     long long gi = (long long)si.bc[0] * G.nb[0] + i;
     long long gj = (long long)si.bc[1] * G.nb[1] + j;

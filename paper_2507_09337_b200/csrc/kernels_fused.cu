@@ -48,9 +48,9 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
   const int pk = push_x_only ? 2 : 1;
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
-  // the F4 scheme variants (HLLC, MC) run their own instantiations (scheme 1)
+  // the F4 scheme variants (HLLC, MC, the expensive EOS) run their own instantiations (scheme 1)
   // so the paper-path kernels keep their register allocation
-  const bool var = G.riemann != 0 || G.limiter != 0;
+  const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
 #define ORCHA_ADV(NB, SCH) \
   fused_advance_n##NB##_s##SCH(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk)
   if (G.nb[0] == 16) return var ? ORCHA_ADV(16, 1) : ORCHA_ADV(16, 0);
@@ -72,7 +72,7 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
   if (!fused_supported(G))
     return launch_stage_ref(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   const int pk = push_x_only ? 2 : 1;
-  const bool var = G.riemann != 0 || G.limiter != 0;
+  const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
 #define ORCHA_STG(NB, SCH) \
   fused_stage_n##NB##_s##SCH(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk)
   if (G.nb[0] == 16) return var ? ORCHA_STG(16, 1) : ORCHA_STG(16, 0);

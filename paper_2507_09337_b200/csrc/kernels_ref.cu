@@ -13,7 +13,7 @@ namespace orcha {
 
 __device__ __forceinline__ Prim load_prim(const double* __restrict__ p, long long cube, const DevGrid& G,
                                           bool* fl) {
-  return eos(p[0], p[cube], p[2 * cube], p[3 * cube], p[4 * cube], G, fl);
+  return eos_var(p[0], p[cube], p[2 * cube], p[3 * cube], p[4 * cube], G, fl);
 }
 
 // D(U) at cell c (offset `o` in the padded cube) along axis AX, accumulated
@@ -33,10 +33,10 @@ __device__ __forceinline__ void accumulate_axis(const double* __restrict__ in, l
   double Fm[5], Fp[5];
   plm_face_var(q[0], q[1], q[2], q[3], G, &L, &R);  // face c-1/2
   if (G.riemann == 1) hllc_store<AX>(L, R, G, Fm, 1);
-  else hll<AX>(L, R, G, Fm);
+  else hll_store_lit<AX>(L, R, G, Fm, 1);
   plm_face_var(q[1], q[2], q[3], q[4], G, &L, &R);  // face c+1/2
   if (G.riemann == 1) hllc_store<AX>(L, R, G, Fp, 1);
-  else hll<AX>(L, R, G, Fp);
+  else hll_store_lit<AX>(L, R, G, Fp, 1);
 #pragma unroll
   for (int v = 0; v < 5; v++) {
     double t = (Fp[v] - Fm[v]) * G.id[AX];
@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(256) stage_ref_kernel(DevGrid G, double* __res
 #pragma unroll
       for (int v = 0; v < 5; v++) un[v * cube] = nw[v];
       bool f2;
-      Prim q = eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
-      s_rec = signal_speed<NDIM>(q, G);
+      Prim q = eos_var(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
+      s_rec = signal_speed_var<NDIM>(q, G);
       g_rec = gcell;
       bool finite = isfinite(nw[0]) && isfinite(nw[1]) && isfinite(nw[2]) && isfinite(nw[3]) && isfinite(nw[4]);
       if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)gcell);

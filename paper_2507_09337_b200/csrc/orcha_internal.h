@@ -31,6 +31,8 @@ struct DevGrid {
   double id[3];     // 1/dx per axis (1/dx computed once)
   double gamma, gm1, ig1, cfl, smallp;  // gm1 = gamma - 1, ig1 = 1/(gamma - 1)
   int riemann, limiter;                 // F4 scheme flags (0 = HLL / minmod)
+  int eos, eos_work;                    // F4 EOS flag (0 = gamma law) and its work multiplier
+  double arad;                          // F4 gas + radiation EOS: radiation constant
 };
 
 // One entry per (slot, neighbour direction); 27 per slot, dir = (oz+1)*9 + (oy+1)*3 + (ox+1).

@@ -140,6 +140,8 @@ extern "C" int32_t orcha_grid_create(const orcha_grid_desc* d, orcha_grid** out)
   if (!(d->gamma > 1.0) || !(d->cfl > 0.0) || !(d->smallp >= 0.0)) return fail(ORCHA_E_ARG, "bad gamma/cfl/smallp");
   if (d->riemann < 0 || d->riemann > 1 || d->limiter < 0 || d->limiter > 1)
     return fail(ORCHA_E_ARG, "riemann must be ORCHA_RIEMANN_HLL/HLLC and limiter ORCHA_LIMITER_MINMOD/MC");
+  if (d->eos < 0 || d->eos > 1 || (d->eos == 1 && (d->eos_work < 1 || !(d->arad >= 0.0))))
+    return fail(ORCHA_E_ARG, "eos must be ORCHA_EOS_GAMMA_LAW or ORCHA_EOS_GAS_RADIATION with eos_work >= 1, arad >= 0");
   orcha_grid* g = new orcha_grid();
   g->desc = *d;
   DevGrid& G = g->dev;
@@ -163,6 +165,9 @@ extern "C" int32_t orcha_grid_create(const orcha_grid_desc* d, orcha_grid** out)
   G.ig1 = 1.0 / (d->gamma - 1.0);
   G.riemann = d->riemann;
   G.limiter = d->limiter;
+  G.eos = d->eos;
+  G.eos_work = d->eos_work < 1 ? 1 : d->eos_work;
+  G.arad = d->arad;
   G.cfl = d->cfl;
   G.smallp = d->smallp;
   *out = g;

@@ -30,7 +30,8 @@ class Grid:
     def __init__(self, ndim: int, nb: Sequence[int], nblk: Sequence[int], ng: int = 4,
                  xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), bc=((0, 0), (0, 0), (0, 0)),
                  gamma: float = 1.4, cfl: float = 0.4, smallp: float = 1e-30, parity: bool = False,
-                 riemann: int = abi.RIEMANN_HLL, limiter: int = abi.LIMITER_MINMOD):
+                 riemann: int = abi.RIEMANN_HLL, limiter: int = abi.LIMITER_MINMOD,
+                 eos: int = abi.EOS_GAMMA_LAW, eos_work: int = 1, arad: float = 0.0):
         self.lib = abi.load(parity)
         self.parity = parity
         nb = list(nb) + [1] * (3 - len(nb))
@@ -47,7 +48,9 @@ class Grid:
         d.ng = ng
         d.gamma, d.cfl, d.smallp = gamma, cfl, smallp
         d.riemann, d.limiter = int(riemann), int(limiter)
+        d.eos, d.eos_work, d.arad = int(eos), int(eos_work), float(arad)
         self.riemann, self.limiter = int(riemann), int(limiter)
+        self.eos, self.eos_work, self.arad = int(eos), int(eos_work), float(arad)
         self.desc = d
         self.ndim, self.nb, self.nblk, self.ng = ndim, tuple(nb), tuple(nblk), ng
         self.N = tuple(nb[a] * nblk[a] for a in range(3))

@@ -11,10 +11,11 @@ import orcha_inputs as inp
 
 
 def make_grid(ndim, nb, nblk, bc=None, xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0), parity=False, riemann=0,
-              limiter=0):
+              limiter=0, eos=0, eos_work=1, arad=0.0):
     from paper_2507_09337_b200 import hydro
     bc = bc or ((0, 0),) * 3
-    return hydro.Grid(ndim, nb, nblk, bc=bc, xmin=xmin, xmax=xmax, parity=parity, riemann=riemann, limiter=limiter)
+    return hydro.Grid(ndim, nb, nblk, bc=bc, xmin=xmin, xmax=xmax, parity=parity, riemann=riemann, limiter=limiter,
+                      eos=eos, eos_work=eos_work, arad=arad)
 
 
 def oracle_grid(g) -> oracle.Grid:
@@ -22,7 +23,7 @@ def oracle_grid(g) -> oracle.Grid:
     return oracle.Grid(N=tuple(g.N[:nd]), xmin=tuple(g.desc.xmin[:nd]) + (0.0,) * (3 - nd),
                        xmax=tuple(g.desc.xmax[:nd]) + (1.0,) * (3 - nd),
                        bc=tuple((g.desc.bc[a][0], g.desc.bc[a][1]) for a in range(3)),
-                       riemann=g.riemann, limiter=g.limiter)
+                       riemann=g.riemann, limiter=g.limiter, eos=g.eos, eos_work=g.eos_work, arad=g.arad)
 
 
 def split_packets(nblocks: int, npackets: int, seed: int = 0, shuffle: bool = False):

@@ -117,6 +117,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference
+def workload_config(world):
+    """The workload both arms report (cfg4 at `world` GPUs)."""
+    px, py, pz = GPU_GRIDS[world]
+    nblk = (BRICK_BLOCKS[0] * px, BRICK_BLOCKS[1] * py, BRICK_BLOCKS[2] * pz)
+    return {"workload": "cfg4: 3D Sedov, 4096 blocks of 16^3 (+4 guards) per GPU, one packet",
+            "global_cells": [nblk[a] * NB[a] for a in range(3)],
+            "blocks_per_gpu": BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2], "gpu_grid": list(GPU_GRIDS[world]),
+            "ng": 4, "gamma": 1.4, "cfl": 0.4, "global_batch": None, "seq_len": None}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle as it stands, on the host cores, one
     bounded sample of the workload per step (a 64^3 sub-box of the same Sedov
@@ -149,8 +159,8 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg4 3D Sedov (oracle sample: 64^3 sub-box per step)", "global_batch": None,
-                       "seq_len": None, "parallelism": "cpu oracle, 1 thread"},
+            "config": dict(workload_config(world), parallelism="cpu oracle, 1 thread (each step: a 64^3 sub-box "
+                                                                           "sample of the same Sedov setup)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"64^3 3D Sedov, {args.steps} timed steps (plain C oracle, -O2 -ffp-contract=off)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -457,11 +467,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (closed-form Sedov IC)",
-            "config": {"workload": "cfg4: 3D Sedov, 4096 blocks of 16^3 (+4 guards) per GPU, one packet",
-                       "global_cells": list(N), "blocks_per_gpu": int(len(ids)), "gpu_grid": list(GPU_GRIDS[world]),
-                       "ng": 4, "gamma": 1.4, "cfl": 0.4, "l2_flush": "not needed: 2.2 GB state per GPU >> 126 MB L2",
-                       "kernel_variant": int(lib.orcha_get_kernel_variant()), "fill_mode": fill_eff,
-                       "global_batch": None, "seq_len": None, "parallelism": f"blocks over {world} GPU(s)"},
+            "config": dict(workload_config(world), l2_flush="not needed: 2.2 GB state per GPU >> 126 MB L2",
+                           kernel_variant=int(lib.orcha_get_kernel_variant()), fill_mode=fill_eff,
+                           parallelism=f"blocks over {world} GPU(s)"),
             "roofline": primary, "roofline_other": other,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
                                        "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},

@@ -17,7 +17,8 @@
 //            one direction (no divergence, no selects); z-faces k+1/2 are
 //            double buffered so the k-1/2 ones survive the plane;
 //   phase 2: the conservative update of the band's cells of plane k, and the
-//            EOS of the next staged plane.
+//            EOS of the next staged plane (measured: doing that EOS in phase
+//            1 instead is slower, 3.44 vs 3.34 ms per cfg4 step).
 // Stage 1 (box: interior + 2-cell ring) writes U1 to an (n+4)^3 scratch;
 // stage 2 (interior) reads it, writes U^{n+1} in place and reduces the CFL
 // signal speed of the new state (fused dt epilogue).  SURVEY 8(a) A5-A9;
@@ -125,10 +126,6 @@ __host__ __device__ constexpr long long u1_cube() {
   return ((long long)(NB + 4) * (NB + 4) * (NB + 4) * 8 + 255) / 256 * 256 / 8;
 }
 
-// PUSH: 0 none, 1 scatter the new state into every same-packet guard
-// (push_cell), 2 into the x-guards only (push_cell_x, gather mode).
-// GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a
-// separate instantiation so the plain kernels carry none of its registers.
 // The x-axis part of push_cell (push.cuh) for a padded target (the states, or
 // the per-stage stage-1 buffers): interior cell (ci, cj, k) feeds the x-guards
 // of the blocks the two cached x entries name (gather fill mode).
@@ -165,6 +162,11 @@ __device__ __forceinline__ void face_flux(const Prim& q0, const Prim& q1, const 
   }
 }
 
+// PUSH: 0 none, 1 scatter the new state into every same-packet guard
+// (push_cell), 2 into the x-guards only (push_x, gather mode).
+// GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a
+// separate instantiation so the plain kernels carry none of its registers.
+// SCH: 0 the paper-path scheme, 1 the grid's F4 flags (see face_flux).
 template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER, int SCH>
 __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,

@@ -192,7 +192,7 @@ def cpu_baseline(seconds_target=15.0):
 
 
 # ----------------------------------------------------------------- GPU arm
-def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world):
+def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_priority=0):
     """End to end with a host-resident mesh (the paper's
     execution model: every cycle each DataPacket is shipped H2D, advanced and
     shipped back): the brick is K z-slab packets whose interiors
@@ -212,7 +212,9 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world):
     pks = [hydro.Packet(g, a) for a in slabs]
     mesh = [torch.from_numpy(inp.sedov_packet(N, NB, a, xmax=(float(px), float(py), float(pz)))).pin_memory()
             for a in slabs]
-    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    # copy streams (priority < 0: their pack / unpack kernels are scheduled
+    # ahead of the pending CTAs of the advance on the compute stream)
+    h2d, d2h = torch.cuda.Stream(priority=copy_priority), torch.cuda.Stream(priority=copy_priority)
     done = [None] * len(pks)
 
     def one():
@@ -270,6 +272,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="orcha", choices=["orcha", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-priority", type=int, default=-1,
+                    help="streamed e2e: CUDA priority of the copy streams (-1 = high)")
     ap.add_argument("--e2e-packets", type=int, default=8,
                     help="streamed e2e: packets (z-slabs of the brick) shipped in and out every step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -436,7 +440,8 @@ def main():
     e2e = None
     e2e_serial = None
     if args.e2e_steps > 0:
-        e2e = streamed_e2e(g, ids, N, px, py, pz, comm, stream, args.e2e_steps, args.e2e_packets, world)
+        e2e = streamed_e2e(g, ids, N, px, py, pz, comm, stream, args.e2e_steps, args.e2e_packets, world,
+                             copy_priority=args.e2e_priority)
     if args.e2e_steps > 0:
         out = torch.empty_like(host).pin_memory()
         torch.cuda.synchronize()

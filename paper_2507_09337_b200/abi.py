@@ -127,6 +127,8 @@ def load(parity: bool = False) -> ctypes.CDLL:
     parity = bool(parity)
     if parity not in _loaded:
         path = LIBS[parity]
+        if not parity and os.environ.get("ORCHA_LIB"):  # experiments: an alternative production build
+            path = os.environ["ORCHA_LIB"]
         if not os.path.exists(path):
             raise ImportError(f"{path} is missing: run `python -m paper_2507_09337_b200.build` "
                               "(the CUDA extension is required; there is no CPU fallback)")

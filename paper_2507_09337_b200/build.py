@@ -92,5 +92,25 @@ def build(force: bool = False, verbose: bool = False) -> list:
     return out
 
 
+def build_experiment(out: str, extra) -> str:
+    """A production library compiled with extra flags (e.g. -D switches of
+    measured alternatives) at `out`; loaded via ORCHA_LIB.  Experiments only."""
+    objdir = tempfile.mkdtemp(prefix="orcha_exp_")
+    flags = VARIANTS["liborcha.so"] + list(extra)
+    pairs = [(src, os.path.join(objdir, os.path.splitext(os.path.basename(src))[0] + ".o")) for src in sources()]
+    with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        for f in [ex.submit(_compile, src, obj, flags) for src, obj in pairs]:
+            f.result()
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *[o for _, o in pairs], "-ldl"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    shutil.rmtree(objdir, ignore_errors=True)
+    return out
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--experiment":
+        print(build_experiment(sys.argv[2], sys.argv[3:]))
+        sys.exit(0)
     print(build(force="--force" in sys.argv, verbose=True))

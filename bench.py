@@ -257,11 +257,22 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ems = float(t.item())
     nbytes = sum(m.numel() for m in mesh) * 8
+    del pks
+    # the host link's own roofline: pinned H2D and D2H of the step's bytes at
+    # once on two streams (scripts/pcie_probe.py), measured here on this box
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
+    import pcie_probe
+    lk = pcie_probe.probe(nbytes=nbytes, reps=3)
+    floor_ms = 2 * nbytes / (lk["bidir_gbs"] * 1e9) * 1e3
     out = {"value": N[0] * N[1] * N[2] / (ems / 1e3), "unit": UNIT,   # N: the global grid (all ranks)
-           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": ems, "packets": len(pks),
+           "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": ems, "packets": len(mesh),
+           "link": {"bound": "pcie", "h2d_gbs": lk["h2d_gbs"], "d2h_gbs": lk["d2h_gbs"],
+                    "bidir_gbs": lk["bidir_gbs"], "floor_ms": floor_ms, "frac": floor_ms / ems,
+                    "note": "floor = the step's H2D + D2H bytes moved concurrently at the measured bidirectional "
+                            "pinned-copy rate; the rest is the serial part of the step (last slab's H2D, fill, "
+                            "dt, first slab's advance + D2H)"},
            "note": f"host-resident mesh, {len(pks)} z-slab packets per GPU shipped in and out every step on copy "
                    "streams overlapping the other packets' compute; step n+1 reads step n's output from the host"}
-    del pks
     return out
 
 

@@ -271,7 +271,7 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
                     "note": "floor = the step's H2D + D2H bytes moved concurrently at the measured bidirectional "
                             "pinned-copy rate; the rest is the serial part of the step (last slab's H2D, fill, "
                             "dt, first slab's advance + D2H)"},
-           "note": f"host-resident mesh, {len(pks)} z-slab packets per GPU shipped in and out every step on copy "
+           "note": f"host-resident mesh, {len(mesh)} z-slab packets per GPU shipped in and out every step on copy "
                    "streams overlapping the other packets' compute; step n+1 reads step n's output from the host"}
     return out
 

@@ -192,7 +192,7 @@ def cpu_baseline(seconds_target=15.0):
 
 
 # ----------------------------------------------------------------- GPU arm
-def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_priority=0):
+def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_priority=0, copy_streams=2):
     """End to end with a host-resident mesh (the paper's
     execution model: every cycle each DataPacket is shipped H2D, advanced and
     shipped back): the brick is K z-slab packets whose interiors
@@ -214,26 +214,46 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
             for a in slabs]
     # copy streams (priority < 0: their pack / unpack kernels are scheduled
     # ahead of the pending CTAs of the advance on the compute stream)
-    h2d, d2h = torch.cuda.Stream(priority=copy_priority), torch.cuda.Stream(priority=copy_priority)
+    # copy_streams > 1: packets alternate over that many H2D and D2H streams,
+    # so one packet's pack / unpack kernel runs while another's copy holds the link
+    h2ds = [torch.cuda.Stream(priority=copy_priority) for _ in range(copy_streams)]
+    d2hs = [torch.cuda.Stream(priority=copy_priority) for _ in range(copy_streams)]
     done = [None] * len(pks)
+
+    # one rank: each slab's dt records right after its pack, its guard fill
+    # right after the next slab's pack (the brick's z faces are outflow, so a
+    # z-slab's guards read only its two neighbour slabs) -- only the last
+    # slab's fill and the dt reduction stay between the last H2D and the
+    # first advance.  Several ranks: the set-wide fill with its exchange.
+    pipelined = comm is None
 
     def one():
         ev_in = []
         for i, p in enumerate(pks):
+            h2d = h2ds[i % len(h2ds)]
             if done[i] is not None:
                 h2d.wait_event(done[i])
             p.pack(mesh[i], h2d)
             e = torch.cuda.Event()
             e.record(h2d)
             ev_in.append(e)
-        for e in ev_in:
-            stream.wait_event(e)
-        hydro.orcha_fill_guardcells(pks, comm, stream)
+            if pipelined:
+                stream.wait_event(e)
+                hydro.orcha_packet_dt_records(p, stream)
+                if i >= 1:
+                    hydro.orcha_fill_guardcells_packet(pks, i - 1, stream)
+        if pipelined:
+            hydro.orcha_fill_guardcells_packet(pks, len(pks) - 1, stream)
+        else:
+            for e in ev_in:
+                stream.wait_event(e)
+            hydro.orcha_fill_guardcells(pks, comm, stream)
         info = hydro.orcha_compute_dt(pks, math.inf, comm, stream)
         for i, p in enumerate(pks):
             hydro.orcha_hydro_advance(p, info.dt, stream)
             e = torch.cuda.Event()
             e.record(stream)
+            d2h = d2hs[i % len(d2hs)]
             d2h.wait_event(e)
             p.unpack(mesh[i], d2h, sync=False)
             e2 = torch.cuda.Event()
@@ -272,7 +292,8 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
                             "pinned-copy rate; the rest is the serial part of the step (last slab's H2D, fill, "
                             "dt, first slab's advance + D2H)"},
            "note": f"host-resident mesh, {len(mesh)} z-slab packets per GPU shipped in and out every step on copy "
-                   "streams overlapping the other packets' compute; step n+1 reads step n's output from the host"}
+                   "streams overlapping the other packets' compute (each slab's dt records and guard fill as soon "
+                   "as it and its neighbours are on the device); step n+1 reads step n's output from the host"}
     return out
 
 
@@ -285,7 +306,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-priority", type=int, default=-1,
                     help="streamed e2e: CUDA priority of the copy streams (-1 = high)")
-    ap.add_argument("--e2e-packets", type=int, default=8,
+    ap.add_argument("--e2e-copy-streams", type=int, default=2,
+                    help="streamed e2e: H2D and D2H streams each (packets alternate over them)")
+    ap.add_argument("--e2e-packets", type=int, default=16,
                     help="streamed e2e: packets (z-slabs of the brick) shipped in and out every step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=None, help="advance kernel variant (0 ref, 1 fused)")
@@ -452,7 +475,7 @@ def main():
     e2e_serial = None
     if args.e2e_steps > 0:
         e2e = streamed_e2e(g, ids, N, px, py, pz, comm, stream, args.e2e_steps, args.e2e_packets, world,
-                             copy_priority=args.e2e_priority)
+                             copy_priority=args.e2e_priority, copy_streams=args.e2e_copy_streams)
     if args.e2e_steps > 0:
         out = torch.empty_like(host).pin_memory()
         torch.cuda.synchronize()

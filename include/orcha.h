@@ -194,6 +194,30 @@ int32_t orcha_packet_unpack_async(const orcha_packet* packet, double* interior, 
 int32_t orcha_fill_guardcells(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
                               void* stream);
 
+/* Streamed packets (the paper overlaps each DataPacket's
+ * transfers with the other packets' work): the two local parts of
+ * a step's preparation, per packet, so they run as soon as that packet's data
+ * is on the device instead of after the whole set arrived.
+ *
+ * orcha_fill_guardcells_packet: the guard fill of orcha_fill_guardcells over
+ * the set `packets` (same tables, same bitwise result), for packets[index]
+ * only.  Every block its guards read must already hold this step's data (the
+ * caller orders `stream` after those packets' packs).  Single device only:
+ * returns ORCHA_E_ARG if a source block lives on another rank (use
+ * orcha_fill_guardcells with a communicator).  Asynchronous.
+ * Errors: ORCHA_E_ARG, ORCHA_E_RANGE, ORCHA_E_CUDA. */
+int32_t orcha_fill_guardcells_packet(orcha_packet* const* packets, int32_t npackets, int32_t index,
+                                     void* stream);
+
+/* orcha_packet_dt_records: the per-packet part of orcha_compute_dt -- the CFL
+ * signal-speed max and its lowest global index over the packet's interior
+ * cells -- computed now on `stream` (asynchronous).  A later
+ * orcha_compute_dt over a set containing the packet only reduces these
+ * records (order its stream after this one); a pack or advance invalidates
+ * them.  Non-positive densities set the sticky status word.
+ * Errors: ORCHA_E_ARG, ORCHA_E_CUDA. */
+int32_t orcha_packet_dt_records(orcha_packet* packet, void* stream);
+
 /* CFL time step over the interior cells of `packets`:
  *   s = ((|u|+c)*idx + (|v|+c)*idy) + (|w|+c)*idz  (inactive axes omitted),
  *   c = sqrt((gamma*p)/rho), dt = cfl / max s; argmax = lowest global g with

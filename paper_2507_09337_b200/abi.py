@@ -30,7 +30,7 @@ EXPORTS = [
     "orcha_comm_create", "orcha_comm_destroy", "orcha_set_kernel_variant", "orcha_get_kernel_variant",
     "orcha_comm_create_local", "orcha_comm_push", "orcha_comm_plan", "orcha_hydro_stage",
     "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push", "orcha_set_fill_mode",
-    "orcha_packet_unpack_async",
+    "orcha_packet_unpack_async", "orcha_fill_guardcells_packet", "orcha_packet_dt_records",
 ]
 
 
@@ -93,6 +93,8 @@ _SIGS = {
     "orcha_packet_unpack_device": (_i32, [_vp, _vp, _vp]),
     "orcha_packet_unpack_async": (_i32, [_vp, _vp, _vp]),
     "orcha_fill_guardcells": (_i32, [_P(_vp), _i32, _vp, _vp]),
+    "orcha_fill_guardcells_packet": (_i32, [_P(_vp), _i32, _i32, _vp]),
+    "orcha_packet_dt_records": (_i32, [_vp, _vp]),
     "orcha_compute_dt": (_i32, [_P(_vp), _i32, _vp, _dbl, _P(orcha_dt_info), _vp]),
     "orcha_hydro_advance": (_i32, [_vp, _dbl, _vp]),
     "orcha_hydro_advance_devdt": (_i32, [_vp, _vp, _vp]),

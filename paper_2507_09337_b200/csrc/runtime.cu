@@ -698,8 +698,10 @@ static int32_t get_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fill
   return ORCHA_OK;
 }
 
+// only >= 0: fill the guards of pk[only] alone (streamed packets: the set's
+// tables, every source resident, no exchange).
 static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer, bool faces_only,
-                         void* stream) {
+                         void* stream, int only = -1) {
   if (!pk || npk < 1) return fail(ORCHA_E_ARG, "no packets");
   if (buffer != 0 && buffer != 1) return fail(ORCHA_E_ARG, "buffer must be 0 (state) or 1 (stage-1 state)");
   for (int q = 0; q < npk; q++) {
@@ -711,6 +713,8 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   int32_t rc = get_plan(pk, npk, comm, &f);
   if (rc) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  if (only >= 0 && f->has_remote)
+    return fail(ORCHA_E_ARG, "a per-packet fill needs every source block resident (no exchange)");
   if (f->has_remote) {
     CommPlan* cp = nullptr;  // cached by the communicator per packet set and buffer
     rc = comm_build_plan(comm, pk, npk, buffer, &cp);
@@ -722,7 +726,7 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   // already current: only the exchange above was needed.
   bool all_pushed = push_enabled();
   for (int q = 0; q < npk; q++)
-    all_pushed &= pk[q]->push_plan == f && (buffer ? pk[q]->u1_pushed : pk[q]->guards_pushed);
+    if (only < 0 || q == only) all_pushed &= pk[q]->push_plan == f && (buffer ? pk[q]->u1_pushed : pk[q]->guards_pushed);
   // gather mode (state only, fused kernels, ONE packet per device; remote
   // sources were exchanged into its own guards above): x-guards only, plus
   // the resident-sourced parts of exchanged rows.  With several packets the advances run one after
@@ -750,12 +754,13 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   // (from 128 packets on: the one-launch kernel pays a dependent descriptor
   // load per cell, ~0.5 ms on 16.8 M cells, which below that is more than the
   // per-packet launches cost)
-  const bool multi = npk >= 128 && !all_pushed && f->d_sf != nullptr;
+  const bool multi = npk >= 128 && !all_pushed && f->d_sf != nullptr && only < 0;
   if (multi) {
     cudaError_t e = launch_fill_multi(G0, buffer ? f->d_sf_u1 : f->d_sf, f->nslots_total, s, faces_only ? 1 : 0);
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   }
   for (int q = 0; q < npk && !multi; q++) {
+    if (only >= 0 && q != only) continue;
     double* dst = buffer ? pk[q]->scratch : pk[q]->state;
     cudaError_t e;
     if (xonly) {
@@ -777,6 +782,7 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
     if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   }
   for (int q = 0; q < npk; q++) {
+    if (only >= 0 && q != only) continue;
     pk[q]->d_push = f->d_push[q];
     pk[q]->d_push_u1 = f->d_push_u1[q];
     pk[q]->push_plan = f;
@@ -799,12 +805,27 @@ extern "C" int32_t orcha_fill_guardcells(orcha_packet* const* pk, int32_t npk, o
   return fill_impl(pk, npk, comm, 0, false, stream);
 }
 
+extern "C" int32_t orcha_fill_guardcells_packet(orcha_packet* const* pk, int32_t npk, int32_t index,
+                                                void* stream) {
+  if (!pk || index < 0 || index >= npk) return fail(ORCHA_E_ARG, "packet index out of range");
+  return fill_impl(pk, npk, nullptr, 0, false, stream, index);
+}
+
 extern "C" int32_t orcha_fill_guardcells_stage(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
                                                int32_t buffer, void* stream) {
   return fill_impl(pk, npk, comm, buffer, true, stream);
 }
 
 // --------------------------------------------------------------- dt ------
+extern "C" int32_t orcha_packet_dt_records(orcha_packet* p, void* stream) {
+  if (!p) return fail(ORCHA_E_ARG, "null packet");
+  cudaError_t e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords, p->status,
+                            (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dt kernel");
+  p->records_valid = true;
+  return ORCHA_OK;
+}
+
 extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, double t_remaining,
                                     orcha_dt_info* info, void* stream) {
   if (!pk || npk < 1 || !info) return fail(ORCHA_E_ARG, "null argument");

@@ -224,6 +224,17 @@ def orcha_fill_guardcells(packets, comm=None, stream=None):
              ctypes.c_void_p(_stream_ptr(stream)))
 
 
+def orcha_fill_guardcells_packet(packets, index: int, stream=None):
+    """Guards of packets[index] only, with the set's tables (streamed packets)."""
+    arr, n = _handles(packets)
+    abi.call(packets[0].lib, "orcha_fill_guardcells_packet", arr, n, int(index), ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def orcha_packet_dt_records(packet: Packet, stream=None):
+    """The packet's CFL records now (the local part of orcha_compute_dt)."""
+    abi.call(packet.lib, "orcha_packet_dt_records", packet.handle, ctypes.c_void_p(_stream_ptr(stream)))
+
+
 def orcha_compute_dt(packets, t_remaining: float = math.inf, comm=None, stream=None, check: bool = True):
     arr, n = _handles(packets)
     lib = packets[0].lib

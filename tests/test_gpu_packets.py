@@ -77,11 +77,16 @@ def test_many_packets_one_launch_fill_and_dt():
     assert np.array_equal(H.gather(g, pk), A)
 
 
-def test_streamed_host_mesh_equals_resident_run():
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_streamed_host_mesh_equals_resident_run(pipelined):
     # SURVEY 8(f) F3 / bench.py's e2e: the mesh lives in pinned host memory as
-    # K packets shipped in (H2D stream), advanced, and shipped out with
-    # orcha_packet_unpack_async (D2H stream) every step, the next step reading
-    # the host mesh -- bitwise the device-resident run
+    # K packets shipped in (H2D streams), advanced, and shipped out with
+    # orcha_packet_unpack_async (D2H streams) every step, the next step reading
+    # the host mesh -- bitwise the device-resident run.  pipelined: each slab's
+    # dt records right after its pack and its guard fill right after the next
+    # slab's pack (orcha_packet_dt_records / orcha_fill_guardcells_packet;
+    # z is not periodic, so a slab's guards read only its neighbour slabs),
+    # packets alternating over two copy streams each way
     import math
     import torch
     from paper_2507_09337_b200 import hydro
@@ -91,27 +96,43 @@ def test_streamed_host_mesh_equals_resident_run():
     slabs = [a for a in np.array_split(np.arange(g.nblocks), 4)]
     pks = [hydro.Packet(g, a) for a in slabs]
     mesh = [torch.from_numpy(inp.to_blocks(U0, g.nb, a)).pin_memory() for a in slabs]
-    comp, h2d, d2h = torch.cuda.current_stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    comp = torch.cuda.current_stream()
+    ns = 2 if pipelined else 1
+    h2ds = [torch.cuda.Stream() for _ in range(ns)]
+    d2hs = [torch.cuda.Stream() for _ in range(ns)]
     done = [None] * len(pks)
     dts = []
     for _ in range(4):
         ev = []
         for i, p in enumerate(pks):
+            h2d = h2ds[i % ns]
             if done[i] is not None:
                 h2d.wait_event(done[i])
             p.pack(mesh[i], h2d)
             e = torch.cuda.Event()
             e.record(h2d)
             ev.append(e)
-        for e in ev:
-            comp.wait_event(e)
-        hydro.orcha_fill_guardcells(pks, None, comp)
+            if pipelined:
+                comp.wait_event(e)
+                hydro.orcha_packet_dt_records(p, comp)
+                if i >= 1:
+                    hydro.orcha_fill_guardcells_packet(pks, i - 1, comp)
+        if pipelined:
+            hydro.orcha_fill_guardcells_packet(pks, len(pks) - 1, comp)
+        else:
+            for e in ev:
+                comp.wait_event(e)
+            hydro.orcha_fill_guardcells(pks, None, comp)
+        n0 = g.lib.orcha_launch_count()
         info = hydro.orcha_compute_dt(pks, math.inf, None, comp)
+        if pipelined:  # the records were computed per packet: only the reduction runs
+            assert g.lib.orcha_launch_count() - n0 == 1
         dts.append(info.dt)
         for i, p in enumerate(pks):
             hydro.orcha_hydro_advance(p, info.dt, comp)
             e = torch.cuda.Event()
             e.record(comp)
+            d2h = d2hs[i % ns]
             d2h.wait_event(e)
             p.unpack(mesh[i], d2h, sync=False)
             e2 = torch.cuda.Event()
@@ -123,3 +144,12 @@ def test_streamed_host_mesh_equals_resident_run():
         out = inp.from_blocks(m.numpy(), g.N, g.nb, a, out)
     assert dts == [x[0] for x in logA]
     assert np.array_equal(out, A)
+
+
+def test_per_packet_fill_arguments():
+    from paper_2507_09337_b200 import abi, hydro
+    g = H.make_grid(3, (8, 8, 8), (2, 2, 2))
+    pks = [hydro.Packet(g, [b]) for b in range(g.nblocks)]
+    for bad in (-1, len(pks)):
+        with pytest.raises(abi.OrchaError, match="ORCHA_E_ARG"):
+            hydro.orcha_fill_guardcells_packet(pks, bad)

@@ -278,18 +278,20 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
     ems = float(t.item())
     nbytes = sum(m.numel() for m in mesh) * 8
     del pks
-    # the host link's own roofline: pinned H2D and D2H of the step's bytes at
-    # once on two streams (scripts/pcie_probe.py), measured here on this box
+    # the host link's own roofline: the step's H2D and D2H bytes over the
+    # same pinned mesh buffers, both directions at once on two streams
+    # (scripts/pcie_probe.py; best of 3), measured here on this box after the
+    # timed region (the mesh contents are no longer needed)
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "scripts"))
     import pcie_probe
-    lk = pcie_probe.probe(nbytes=nbytes, reps=3)
+    lk = pcie_probe.probe_buffers(mesh, reps=3)
     floor_ms = 2 * nbytes / (lk["bidir_gbs"] * 1e9) * 1e3
     out = {"value": N[0] * N[1] * N[2] / (ems / 1e3), "unit": UNIT,   # N: the global grid (all ranks)
            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": ems, "packets": len(mesh),
            "link": {"bound": "pcie", "h2d_gbs": lk["h2d_gbs"], "d2h_gbs": lk["d2h_gbs"],
                     "bidir_gbs": lk["bidir_gbs"], "floor_ms": floor_ms, "frac": floor_ms / ems,
-                    "note": "floor = the step's H2D + D2H bytes moved concurrently at the measured bidirectional "
-                            "pinned-copy rate; the rest is the serial part of the step (last slab's H2D, fill, "
+                    "note": "floor = the step's H2D + D2H bytes moved concurrently at the bidirectional rate "
+                            "measured over the same pinned mesh buffers; the rest is the serial part of the step (last slab's H2D, fill, "
                             "dt, first slab's advance + D2H)"},
            "note": f"host-resident mesh, {len(mesh)} z-slab packets per GPU shipped in and out every step on copy "
                    "streams overlapping the other packets' compute (each slab's dt records and guard fill as soon "
@@ -303,7 +305,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="orcha", choices=["orcha", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-priority", type=int, default=-1,
                     help="streamed e2e: CUDA priority of the copy streams (-1 = high)")
     ap.add_argument("--e2e-copy-streams", type=int, default=2,

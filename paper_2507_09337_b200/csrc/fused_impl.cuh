@@ -39,6 +39,15 @@
 #include "push.cuh"
 #include "reduce.cuh"
 
+// phase-2 converts by the warps without update cells only (ORCHA_CONV_SPLIT=0: by all threads)
+#ifndef ORCHA_CONV_SPLIT
+#define ORCHA_CONV_SPLIT 1
+#endif
+// ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
+#ifndef ORCHA_ISSUE_LAST
+#define ORCHA_ISSUE_LAST 0
+#endif
+
 namespace orcha {
 
 // ------------------------------------------------------------ PTX helpers --
@@ -267,11 +276,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     }
   };
   auto wait_plane = [&](int p) { mbar_wait(&bar[p % NS], (p / NS) & 1); };
-  auto convert = [&](int p) {  // EOS in place over the staged band of plane p
+  // EOS in place over the staged band of plane p: cells c0, c0 + nthr, ...
+  auto convert = [&](int p, int c0 = -1, int nthr = Gm::NT) {
     double* Q = ring + (p % NS) * 5 * BAND;
     const int z = Gm::K0 - 2 + p;
     unsigned long long hits = 0;
-    for (int c = tid; c < BAND; c += NT) {
+    for (int c = (c0 < 0 ? tid : c0); c < BAND; c += nthr) {
       bool fl;
       int r = c / IPX;
       double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
@@ -368,7 +378,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   }
 
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
-  if (tid < 32)
+  const bool issuer = ORCHA_ISSUE_LAST ? warp == Gm::NW - 1 : warp == 0;  // the warp that stages planes
+  if (issuer)
     for (int p = 0; p < NS; p++) issue(p);
   if (GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
   for (int p = 0; p < 5; p++) {
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   __syncthreads();
   for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
   __syncthreads();
-  if (tid < 32) issue(5);  // into the slot of plane 0
+  if (issuer) issue(5);  // into the slot of plane 0
 
   double s_rec = -DBL_MAX;
   long long g_rec = LLONG_MAX;
@@ -429,10 +440,18 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     __syncthreads();
     // phase 2: stage plane it+6 into the slot of plane it+1 (read for the
     // last time in phase 1), convert plane it+5, update the band's cells
-    if (tid < 32) issue(it + 6);
+    if (issuer) issue(it + 6);
     if (it + 5 < Gm::NPLANES) {
-      wait_plane(it + 5);
-      convert(it + 5);
+      constexpr int UW = (Gm::FZ + 31) / 32;  // warps with update cells
+      if constexpr (ORCHA_CONV_SPLIT && Gm::NW - UW >= 2) {
+        if (warp >= UW) {
+          wait_plane(it + 5);
+          convert(it + 5, tid - UW * 32, NT - UW * 32);
+        }
+      } else {
+        wait_plane(it + 5);
+        convert(it + 5);
+      }
     }
     if (upd) {
       const double* fz_prev = Fz + ((it + 1) & 1) * 5 * Gm::FZ;

@@ -316,6 +316,8 @@ def main():
     ap.add_argument("--variant", type=int, default=None, help="advance kernel variant (0 ref, 1 fused)")
     ap.add_argument("--method", default="telescoped", choices=["telescoped", "per-stage"],
                     help="RK2 step: the paper's telescoped step (default) or the per-stage F1 variant")
+    ap.add_argument("--dt-mode", default="device", choices=["device", "host"],
+                    help="dt kept on the device (orcha_compute_dt_device, default) or returned to the host every step")
     ap.add_argument("--no-variants", action="store_true", help="skip the per-stage measurement beside the main line")
     ap.add_argument("--fill-mode", default="gather", choices=["gather", "full"],
                     help="guard fill: gather (x-guards only, y/z rows staged from their owners; default) or full")
@@ -372,16 +374,28 @@ def main():
 
     adv_ev = []
 
+    # dt on the device (default): orcha_compute_dt_device -> the *_devdt step
+    # calls, no host synchronization inside the time loop; --dt-mode host:
+    # orcha_compute_dt returns dt to the host every step (the paper's MPI model)
+    clock = hydro.DevClock(0.0, math.inf) if args.dt_mode == "device" else None
+
     def step(record=False, method=args.method):
         if method == "per-stage":
             hydro.orcha_fill_guardcells_stage([pk], 0, comm, stream)
         else:
             hydro.orcha_fill_guardcells([pk], comm, stream)
-        info = hydro.orcha_compute_dt([pk], math.inf, comm, stream)
+        info = None
+        if clock is None:
+            info = hydro.orcha_compute_dt([pk], math.inf, comm, stream)
+        else:
+            hydro.orcha_compute_dt_device([pk], clock, comm, stream)
         if record:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        hydro.step([pk], info.dt, comm, stream, method)
+        if clock is None:
+            hydro.step([pk], info.dt, comm, stream, method)
+        else:
+            hydro.step_devdt([pk], clock.dt_tensor, comm, stream, method)
         if record:
             b.record(stream)
             adv_ev.append((a, b))
@@ -514,7 +528,7 @@ def main():
             "roofline": primary, "roofline_other": other,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
                                        "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},
-            "advance_ms": adv_ms, "method": args.method, "variants": variants,
+            "advance_ms": adv_ms, "method": args.method, "dt_mode": args.dt_mode, "variants": variants,
             "clocks": clk, "gpu_launches": int(launches), "e2e": e2e, "e2e_serial": e2e_serial,
             "floor_hits": fh, "nonphysical_first_cell": bad,
         }

@@ -107,6 +107,22 @@ typedef struct {
   int32_t nonphysical;/* 1 if a non-positive/non-finite density was met */
 } orcha_dt_info;
 
+/* Device-resident clock of orcha_compute_dt_device (caller-owned DEVICE
+ * memory, 8-byte aligned, 64 bytes).  The caller initialises t, t_end (and
+ * steps) before the first step; every call writes dt, smax, argmax, tag and
+ * nonphysical as orcha_compute_dt reports them and advances t by dt. */
+typedef struct {
+  double t;           /* simulation time (advanced by dt on every call) */
+  double t_end;       /* end time: dt is clamped to t_end - t (tag CLAMP) */
+  double dt;          /* selected time step (pass &clock->dt to *_devdt) */
+  double smax;        /* max signal speed sum */
+  int64_t argmax;     /* lowest global cell index g with s == smax */
+  int32_t tag;        /* ORCHA_DT_CFL or ORCHA_DT_CLAMP */
+  int32_t nonphysical;/* 1 if a non-positive/non-finite density was met */
+  int64_t steps;      /* calls so far (incremented on every call) */
+  int64_t reserved;
+} orcha_dev_clock;
+
 /* ------------------------------------------------------------- grid ---- */
 
 /* Validate `desc` and create a grid handle (host only, no device work).
@@ -230,6 +246,21 @@ int32_t orcha_packet_dt_records(orcha_packet* packet, void* stream);
  * non-positive/non-finite density was met (info still filled). */
 int32_t orcha_compute_dt(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
                          double t_remaining, orcha_dt_info* info, void* stream);
+
+/* orcha_compute_dt with the result kept on the device (no host
+ * synchronization, so a time loop of fill -> dt -> advance runs ahead of the
+ * host and can be captured in a CUDA graph): the same records, the same
+ * cross-rank rule (with `comm`: an NCCL allgather of one 32-byte record per
+ * rank, reduced on the device) and the same IEEE operations as
+ * orcha_compute_dt, so dt is bitwise identical; written to `d_clock`
+ * (orcha_dev_clock), whose `dt` feeds orcha_hydro_advance_devdt.  With
+ * several packets a small table of the packets' records is uploaded first
+ * (not capturable).  Non-physical states are reported in
+ * d_clock->nonphysical and by the next synchronizing call.
+ * Errors: ORCHA_E_ARG (null arguments; LOCAL virtual-rank communicators),
+ * ORCHA_E_CUDA, ORCHA_E_NCCL. */
+int32_t orcha_compute_dt_device(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm,
+                                orcha_dev_clock* d_clock, void* stream);
 
 /* One full telescoped SSP-RK2 step of every block of the packet, in place
  * (sec 6: explicit finite volume with a guard-cell halo, "2nd-order

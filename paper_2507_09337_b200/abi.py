@@ -31,6 +31,7 @@ EXPORTS = [
     "orcha_comm_create_local", "orcha_comm_push", "orcha_comm_plan", "orcha_hydro_stage",
     "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push", "orcha_set_fill_mode",
     "orcha_packet_unpack_async", "orcha_fill_guardcells_packet", "orcha_packet_dt_records",
+    "orcha_compute_dt_device",
 ]
 
 
@@ -71,6 +72,20 @@ class orcha_dt_info(ctypes.Structure):
     ]
 
 
+class orcha_dev_clock(ctypes.Structure):
+    _fields_ = [
+        ("t", ctypes.c_double),
+        ("t_end", ctypes.c_double),
+        ("dt", ctypes.c_double),
+        ("smax", ctypes.c_double),
+        ("argmax", ctypes.c_int64),
+        ("tag", ctypes.c_int32),
+        ("nonphysical", ctypes.c_int32),
+        ("steps", ctypes.c_int64),
+        ("reserved", ctypes.c_int64),
+    ]
+
+
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
@@ -98,6 +113,7 @@ _SIGS = {
     "orcha_compute_dt": (_i32, [_P(_vp), _i32, _vp, _dbl, _P(orcha_dt_info), _vp]),
     "orcha_hydro_advance": (_i32, [_vp, _dbl, _vp]),
     "orcha_hydro_advance_devdt": (_i32, [_vp, _vp, _vp]),
+    "orcha_compute_dt_device": (_i32, [_P(_vp), _i32, _vp, _vp, _vp]),
     "orcha_packet_counters": (_i32, [_vp, _P(_i64), _P(_i64), _vp]),
     "orcha_build_is_parity": (_i32, []),
     "orcha_launch_count": (_i64, []),

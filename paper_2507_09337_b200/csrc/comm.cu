@@ -429,13 +429,6 @@ int32_t comm_exchange(orcha_comm* c, CommPlan* P, cudaStream_t s) {
   return unpack_all(c, P, s);
 }
 
-struct GatherRec {
-  double s;
-  long long g;
-  long long bad;
-  long long pad;
-};
-
 int32_t comm_allreduce_dt(orcha_comm* c, double* smax, long long* g, bool* bad, cudaStream_t s) {
   if (c->local || c->nranks == 1) return ORCHA_OK;  // LOCAL: the caller reduces over all virtual ranks
   GatherRec mine{*smax, *g, *bad ? 1 : 0, 0};
@@ -458,6 +451,26 @@ int32_t comm_allreduce_dt(orcha_comm* c, double* smax, long long* g, bool* bad, 
   *smax = sm;
   *g = gm;
   *bad = b;
+  return ORCHA_OK;
+}
+
+// Device-resident variant: this rank's record (device, 32 B) allgathered into
+// the communicator's buffer, no host round trip; returns the gathered array.
+int32_t comm_allgather_dt_device(orcha_comm* c, const GatherRec* mine, const GatherRec** all, int* nall,
+                                 cudaStream_t s) {
+  if (c->local) return fail(ORCHA_E_ARG, "orcha_compute_dt_device: LOCAL (virtual-rank) communicators are not supported");
+  char* base = (char*)c->d_gather;
+  cudaError_t e = cudaMemcpyAsync(base, mine, 32, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "dt record copy");
+  if (c->nranks > 1) {
+    ncclResult_t r = nccl().AllGather(base, base + 32, 32, ncclUint8, c->nc, s);
+    if (r != ncclSuccess) return nccl_fail(r, "dt allgather");
+    *all = (const GatherRec*)(base + 32);
+    *nall = c->nranks;
+  } else {
+    *all = (const GatherRec*)base;
+    *nall = 1;
+  }
   return ORCHA_OK;
 }
 

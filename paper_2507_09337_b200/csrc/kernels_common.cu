@@ -276,6 +276,49 @@ cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out
   return cudaGetLastError();
 }
 
+__global__ void dt_gather_rec_kernel(const DtRecord* r, const DevStatus* st, GatherRec* out) {
+  out->s = r->s;
+  out->g = r->g;
+  out->bad = st->first_bad != ~0ull ? 1 : 0;
+  out->pad = 0;
+}
+
+cudaError_t launch_dt_gather_rec(const DtRecord* r, const DevStatus* st, GatherRec* out, cudaStream_t s) {
+  dt_gather_rec_kernel<<<1, 1, 0, s>>>(r, st, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// The host rule of orcha_compute_dt on the device (same IEEE operations, so
+// bitwise the same dt): combine the ranks' records (max s, ties -> lowest g),
+// dt = cfl / s_max, then the t_end clamp; clock->t advances by dt.
+__global__ void dt_finish_kernel(const GatherRec* all, int nall, double cfl, DevClock* c) {
+  double sm = all[0].s;
+  long long gm = all[0].g;
+  long long bad = 0;
+  for (int q = 0; q < nall; q++) {
+    if (dt_better(all[q].s, all[q].g, sm, gm)) { sm = all[q].s; gm = all[q].g; }
+    bad |= all[q].bad;
+  }
+  double dt = cfl / sm;
+  int tag = 0;
+  const double rem = c->t_end - c->t;
+  if (rem < dt) { dt = rem; tag = 1; }
+  c->dt = dt;
+  c->smax = sm;
+  c->argmax = gm;
+  c->tag = tag;
+  c->nonphysical = bad ? 1 : 0;
+  c->t = c->t + dt;
+  c->steps = c->steps + 1;
+}
+
+cudaError_t launch_dt_finish(const GatherRec* all, int nall, double cfl, void* clock, cudaStream_t s) {
+  dt_finish_kernel<<<1, 1, 0, s>>>(all, nall, cfl, (DevClock*)clock);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Several packets at once: the records of every packet (same rule, so the
 // result equals the host-side combination of the per-packet reductions) and
 // the packets' sticky status words (lowest first_bad, summed floor hits).

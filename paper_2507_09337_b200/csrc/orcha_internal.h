@@ -65,6 +65,16 @@ struct DtRecord {
   long long g;
 };
 
+using DevClock = orcha_dev_clock;
+
+// Cross-rank dt record (32 bytes, allgathered by NCCL).
+struct GatherRec {
+  double s;
+  long long g;
+  long long bad;
+  long long pad;
+};
+
 // Multi-packet dt reduction: one packet's records and status word.
 struct PacketDt {
   const DtRecord* rec;
@@ -109,6 +119,7 @@ struct orcha_packet {
   double* scratch;             // caller-owned: U1 cubes, then tail
   orcha::DevStatus* status;    // in scratch tail
   orcha::DtRecord* result;     // in scratch tail (1 record)
+  orcha::GatherRec* d_grec;    // in scratch tail, 64 B after result (orcha_compute_dt_device)
   orcha::DtRecord* records;    // in scratch tail
   long long records_cap;
   long long nrecords;          // records written by the last advance/dt kernel
@@ -161,6 +172,11 @@ cudaError_t launch_status_reset(DevStatus* st, cudaStream_t s);
 cudaError_t launch_dt(const DevGrid& G, const double* state, int nslots, const SlotInfo* slots,
                       DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s);
 cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out, cudaStream_t s);
+// Device-resident dt (orcha_compute_dt_device): the reduced record and
+// status -> this rank's GatherRec; then (after an optional allgather of
+// nall records) dt, tag and the clock update in `clock` (orcha_dev_clock).
+cudaError_t launch_dt_gather_rec(const DtRecord* r, const DevStatus* st, GatherRec* out, cudaStream_t s);
+cudaError_t launch_dt_finish(const GatherRec* all, int nall, double cfl, void* clock, cudaStream_t s);
 cudaError_t launch_dt_reduce_multi(const PacketDt* pd, int npk, DtRecord* out, DevStatus* out_st, cudaStream_t s);
 cudaError_t launch_fill_multi(const DevGrid& G, const SlotFill* sf, long long nslots, cudaStream_t s,
                               int faces_only);

@@ -239,7 +239,8 @@ static void free_plan_tables(FillPlan* f) {
 struct DtPlan {
   std::vector<orcha_packet*> packets;
   PacketDt* d_pd = nullptr;
-  DtRecord* d_out = nullptr;   // followed by a DevStatus
+  DtRecord* d_out = nullptr;   // followed by a DevStatus; + 64 B: a GatherRec (orcha_compute_dt_device)
+  GatherRec* d_rec = nullptr;
 };
 static std::vector<DtPlan*> g_dtplans;
 static std::mutex g_plan_mu;
@@ -287,7 +288,8 @@ static int32_t get_dtplan(orcha_packet* const* pk, int npk, DtPlan** out) {
   DtPlan* d = new DtPlan();
   d->packets.assign(pk, pk + npk);
   cudaError_t e = cudaMalloc(&d->d_pd, npk * sizeof(PacketDt));
-  if (e == cudaSuccess) e = cudaMalloc(&d->d_out, sizeof(DtRecord) + sizeof(DevStatus));
+  if (e == cudaSuccess) e = cudaMalloc(&d->d_out, 64 + sizeof(GatherRec));
+  if (e == cudaSuccess) d->d_rec = (GatherRec*)((char*)d->d_out + 64);
   if (e != cudaSuccess) {
     cudaFree(d->d_pd);
     delete d;
@@ -320,6 +322,7 @@ extern "C" int32_t orcha_packet_create(const orcha_grid* g, int32_t n, const int
   char* base = (char*)d_scratch;
   p->status = (DevStatus*)(base + t.status_off);
   p->result = (DtRecord*)(base + t.result_off);
+  p->d_grec = (GatherRec*)(base + t.result_off + 64);
   p->records = (DtRecord*)(base + t.records_off);
   p->records_cap = records_capacity(g->dev, n);
   p->nrecords = 0;
@@ -889,6 +892,61 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
   info->tag = tag;
   info->nonphysical = bad ? 1 : 0;
   if (bad) return fail(ORCHA_E_NONPHYSICAL, "non-physical state (rho <= 0 or non-finite) in a packet (NonPositiveState)");
+  return ORCHA_OK;
+}
+
+namespace orcha {
+int32_t comm_allgather_dt_device(orcha_comm* c, const GatherRec* mine, const GatherRec** all, int* nall,
+                                 cudaStream_t s);
+}
+
+extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
+                                           orcha_dev_clock* d_clock, void* stream) {
+  if (!pk || npk < 1 || !d_clock) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int q = 0; q < npk; q++) {
+    orcha_packet* p = pk[q];
+    if (!p) return fail(ORCHA_E_ARG, "null packet");
+    if (!p->records_valid) {
+      cudaError_t e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords,
+                                p->status, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dt kernel");
+      p->records_valid = true;
+    }
+  }
+  const DtRecord* r = nullptr;
+  const DevStatus* st = nullptr;
+  GatherRec* mine = nullptr;
+  cudaError_t e;
+  if (npk > 1) {
+    DtPlan* dp = nullptr;
+    int32_t rc = get_dtplan(pk, npk, &dp);
+    if (rc) return rc;
+    std::vector<PacketDt> h(npk);
+    for (int q = 0; q < npk; q++) h[q] = PacketDt{pk[q]->records, pk[q]->nrecords, pk[q]->status};
+    e = cudaMemcpyAsync(dp->d_pd, h.data(), npk * sizeof(PacketDt), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = launch_dt_reduce_multi(dp->d_pd, npk, dp->d_out, (DevStatus*)(dp->d_out + 1), s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt reduce");
+    r = dp->d_out;
+    st = (const DevStatus*)(dp->d_out + 1);
+    mine = dp->d_rec;
+  } else {
+    e = launch_dt_reduce(pk[0]->records, pk[0]->nrecords, pk[0]->result, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt reduce");
+    r = pk[0]->result;
+    st = pk[0]->status;
+    mine = pk[0]->d_grec;
+  }
+  e = launch_dt_gather_rec(r, st, mine, s);
+  if (e != cudaSuccess) return cuda_fail(e, "dt record");
+  const GatherRec* all = mine;
+  int nall = 1;
+  if (comm) {
+    int32_t rc = comm_allgather_dt_device(comm, mine, &all, &nall, s);
+    if (rc) return rc;
+  }
+  e = launch_dt_finish(all, nall, pk[0]->grid->dev.cfl, d_clock, s);
+  if (e != cudaSuccess) return cuda_fail(e, "dt finish");
   return ORCHA_OK;
 }
 

@@ -250,6 +250,35 @@ def orcha_hydro_advance(packet: Packet, dt: float, stream=None):
     abi.call(packet.lib, "orcha_hydro_advance", packet.handle, float(dt), ctypes.c_void_p(_stream_ptr(stream)))
 
 
+class DevClock:
+    """orcha_dev_clock in device memory (a 64-byte torch buffer): t, t_end
+    set here; orcha_compute_dt_device writes dt and advances t on the device."""
+
+    def __init__(self, t: float = 0.0, t_end: float = math.inf, device="cuda"):
+        assert ctypes.sizeof(abi.orcha_dev_clock) == 64
+        self.buf = torch.zeros(8, dtype=torch.float64, device=device)
+        self.buf[0] = t
+        self.buf[1] = t_end
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    @property
+    def dt_tensor(self) -> torch.Tensor:
+        return self.buf[2:3]  # &clock->dt, for orcha_hydro_advance_devdt
+
+    def read(self) -> "abi.orcha_dev_clock":
+        h = self.buf.cpu().numpy().tobytes()
+        return abi.orcha_dev_clock.from_buffer_copy(h)
+
+
+def orcha_compute_dt_device(packets, clock: DevClock, comm=None, stream=None):
+    arr, n = _handles(packets)
+    abi.call(packets[0].lib, "orcha_compute_dt_device", arr, n, comm.handle if comm is not None else None,
+             ctypes.c_void_p(clock.ptr), ctypes.c_void_p(_stream_ptr(stream)))
+
+
 def orcha_hydro_advance_devdt(packet: Packet, d_dt: torch.Tensor, stream=None):
     assert d_dt.dtype == torch.float64 and d_dt.is_cuda
     abi.call(packet.lib, "orcha_hydro_advance_devdt", packet.handle, ctypes.c_void_p(d_dt.data_ptr()),
@@ -289,6 +318,27 @@ def step(packets, dt: float, comm=None, stream=None, method: str = "telescoped")
         raise ValueError(method)
 
 
+def orcha_hydro_stage_devdt(packet: Packet, stage: int, d_dt: torch.Tensor, stream=None):
+    assert d_dt.dtype == torch.float64 and d_dt.is_cuda
+    abi.call(packet.lib, "orcha_hydro_stage_devdt", packet.handle, int(stage), ctypes.c_void_p(d_dt.data_ptr()),
+             ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def step_devdt(packets, d_dt: torch.Tensor, comm=None, stream=None, method: str = "telescoped"):
+    """step() with dt read from device memory (e.g. DevClock.dt_tensor)."""
+    if method == "telescoped":
+        for p in packets:
+            orcha_hydro_advance_devdt(p, d_dt, stream)
+    elif method == "per-stage":
+        for p in packets:
+            orcha_hydro_stage_devdt(p, 1, d_dt, stream)
+        orcha_fill_guardcells_stage(packets, 1, comm, stream)
+        for p in packets:
+            orcha_hydro_stage_devdt(p, 2, d_dt, stream)
+    else:
+        raise ValueError(method)
+
+
 def run(packets, nsteps: Optional[int] = None, t_end: float = math.inf, comm=None, stream=None,
         method: str = "telescoped"):
     """The driver loop of SURVEY 8(c): fill -> dt (then t_end clamp) -> step,
@@ -307,3 +357,30 @@ def run(packets, nsteps: Optional[int] = None, t_end: float = math.inf, comm=Non
         n += 1
         log.append((info.dt, info.smax, info.argmax, info.tag))
     return t, n, log
+
+
+def run_device(packets, nsteps: int, t_end: float = math.inf, comm=None, stream=None, record: bool = True,
+               method: str = "telescoped"):
+    """The same loop with dt kept on the device (orcha_compute_dt_device ->
+    the *_devdt step calls): no host synchronization per step.  Returns (clock, log) -- log = [(dt, smax, argmax, tag)] per step,
+    read after the loop (record=False: none)."""
+    clock = DevClock(0.0, t_end)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    hist = torch.empty((nsteps, 8), dtype=torch.float64, device=clock.buf.device) if record else None
+    for n in range(nsteps):
+        if method == "per-stage":
+            orcha_fill_guardcells_stage(packets, 0, comm, s)
+        else:
+            orcha_fill_guardcells(packets, comm, s)
+        orcha_compute_dt_device(packets, clock, comm, s)
+        step_devdt(packets, clock.dt_tensor, comm, s, method)
+        if record:
+            with torch.cuda.stream(s):
+                hist[n].copy_(clock.buf)
+    s.synchronize()
+    log = []
+    if record:
+        for row in hist.cpu().numpy():
+            c = abi.orcha_dev_clock.from_buffer_copy(row.tobytes())
+            log.append((c.dt, c.smax, c.argmax, c.tag))
+    return clock, log

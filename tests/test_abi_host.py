@@ -120,7 +120,8 @@ def test_advance_requires_fill_is_documented():
 def test_ctypes_structs_match_the_header(tmp_path):
     # the binding's struct layouts equal the C compiler's for include/orcha.h
     # (sizes and every field offset), so the marshalling cannot drift
-    fields = {"orcha_grid_desc": abi.orcha_grid_desc, "orcha_dt_info": abi.orcha_dt_info}
+    fields = {"orcha_grid_desc": abi.orcha_grid_desc, "orcha_dt_info": abi.orcha_dt_info,
+              "orcha_dev_clock": abi.orcha_dev_clock}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "orcha.h"', "int main(void) {"]
     for name, cls in fields.items():
         lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')

@@ -226,6 +226,7 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
     # slab's fill and the dt reduction stay between the last H2D and the
     # first advance.  Several ranks: the set-wide fill with its exchange.
     pipelined = comm is None
+    clock = hydro.DevClock(0.0, math.inf)
 
     def one():
         ev_in = []
@@ -248,9 +249,9 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
             for e in ev_in:
                 stream.wait_event(e)
             hydro.orcha_fill_guardcells(pks, comm, stream)
-        info = hydro.orcha_compute_dt(pks, math.inf, comm, stream)
+        hydro.orcha_compute_dt_device(pks, clock, comm, stream)  # dt stays on the device
         for i, p in enumerate(pks):
-            hydro.orcha_hydro_advance(p, info.dt, stream)
+            hydro.orcha_hydro_advance_devdt(p, clock.dt_tensor, stream)
             e = torch.cuda.Event()
             e.record(stream)
             d2h = d2hs[i % len(d2hs)]

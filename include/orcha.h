@@ -254,8 +254,9 @@ int32_t orcha_compute_dt(orcha_packet* const* packets, int32_t npackets, orcha_c
  * rank, reduced on the device) and the same IEEE operations as
  * orcha_compute_dt, so dt is bitwise identical; written to `d_clock`
  * (orcha_dev_clock), whose `dt` feeds orcha_hydro_advance_devdt.  With
- * several packets a small table of the packets' records is uploaded first
- * (not capturable).  Non-physical states are reported in
+ * several packets a small table of the packets' records is uploaded when it
+ * changed since the last call (the first call; steady-state calls only
+ * enqueue kernels and may be captured in a CUDA graph).  Non-physical states are reported in
  * d_clock->nonphysical and by the next synchronizing call.
  * Errors: ORCHA_E_ARG (null arguments; LOCAL virtual-rank communicators),
  * ORCHA_E_CUDA, ORCHA_E_NCCL. */

@@ -241,7 +241,24 @@ struct DtPlan {
   PacketDt* d_pd = nullptr;
   DtRecord* d_out = nullptr;   // followed by a DevStatus; + 64 B: a GatherRec (orcha_compute_dt_device)
   GatherRec* d_rec = nullptr;
+  std::vector<PacketDt> uploaded;  // the table in d_pd (re-uploaded only when it changes)
 };
+
+// The packets' record table for the multi-packet reduction, uploaded only
+// when it differs from the last upload (so steady-state calls enqueue
+// kernels only: capturable in a CUDA graph).
+static cudaError_t upload_dt_table(DtPlan* dp, orcha_packet* const* pk, int npk, cudaStream_t s) {
+  std::vector<PacketDt> h(npk);
+  for (int q = 0; q < npk; q++) h[q] = PacketDt{pk[q]->records, pk[q]->nrecords, pk[q]->status};
+  bool same = dp->uploaded.size() == h.size();
+  for (int q = 0; same && q < npk; q++)
+    same = dp->uploaded[q].rec == h[q].rec && dp->uploaded[q].n == h[q].n && dp->uploaded[q].st == h[q].st;
+  if (same) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(dp->d_pd, h.data(), npk * sizeof(PacketDt), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // h is a temporary
+  if (e == cudaSuccess) dp->uploaded = h;
+  return e;
+}
 static std::vector<DtPlan*> g_dtplans;
 static std::mutex g_plan_mu;
 static std::vector<FillPlan*> g_plans;
@@ -851,10 +868,8 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
     DtPlan* dp = nullptr;
     int32_t rc = get_dtplan(pk, npk, &dp);
     if (rc) return rc;
-    std::vector<PacketDt> h(npk);
-    for (int q = 0; q < npk; q++) h[q] = PacketDt{pk[q]->records, pk[q]->nrecords, pk[q]->status};
     struct { DtRecord r; DevStatus st; } o;
-    cudaError_t e = cudaMemcpyAsync(dp->d_pd, h.data(), npk * sizeof(PacketDt), cudaMemcpyHostToDevice, s);
+    cudaError_t e = upload_dt_table(dp, pk, npk, s);
     if (e == cudaSuccess) e = launch_dt_reduce_multi(dp->d_pd, npk, dp->d_out, (DevStatus*)(dp->d_out + 1), s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&o, dp->d_out, sizeof(DtRecord) + sizeof(DevStatus),
                                               cudaMemcpyDeviceToHost, s);
@@ -922,9 +937,7 @@ extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk,
     DtPlan* dp = nullptr;
     int32_t rc = get_dtplan(pk, npk, &dp);
     if (rc) return rc;
-    std::vector<PacketDt> h(npk);
-    for (int q = 0; q < npk; q++) h[q] = PacketDt{pk[q]->records, pk[q]->nrecords, pk[q]->status};
-    e = cudaMemcpyAsync(dp->d_pd, h.data(), npk * sizeof(PacketDt), cudaMemcpyHostToDevice, s);
+    e = upload_dt_table(dp, pk, npk, s);
     if (e == cudaSuccess) e = launch_dt_reduce_multi(dp->d_pd, npk, dp->d_out, (DevStatus*)(dp->d_out + 1), s);
     if (e != cudaSuccess) return cuda_fail(e, "dt reduce");
     r = dp->d_out;

@@ -384,3 +384,28 @@ def run_device(packets, nsteps: int, t_end: float = math.inf, comm=None, stream=
             c = abi.orcha_dev_clock.from_buffer_copy(row.tobytes())
             log.append((c.dt, c.smax, c.argmax, c.tag))
     return clock, log
+
+
+def capture_steps(packets, clock: DevClock, nsteps: int, comm=None, method: str = "telescoped"):
+    """A CUDA graph of `nsteps` device-dt time steps (fill -> orcha_compute_dt_device
+    -> *_devdt step): the host state machine must be in steady state (call
+    this after at least one plain device-dt step, so the fill launches
+    nothing new and every kernel's attributes are set); each replay advances
+    the packets and the device clock by `nsteps` steps (run two plain steps
+    after a pack first: the first one's dt records come from the dt kernel,
+    later ones from the fused epilogue).  Single rank only (NCCL
+    calls inside a capture need a graph-aware communicator)."""
+    assert comm is None, "capture_steps: single rank"
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(nsteps):
+            if method == "per-stage":
+                orcha_fill_guardcells_stage(packets, 0, None, side)
+            else:
+                orcha_fill_guardcells(packets, None, side)
+            orcha_compute_dt_device(packets, clock, None, side)
+            step_devdt(packets, clock.dt_tensor, None, side, method)
+    torch.cuda.current_stream().wait_stream(side)
+    return g

@@ -98,3 +98,29 @@ def test_device_dt_reports_nonphysical_state():
     hydro.orcha_fill_guardcells(pk)
     hydro.orcha_compute_dt_device(pk, clock)
     assert clock.read().nonphysical == 1
+
+
+@pytest.mark.parametrize("npackets", [1, 2])
+def test_cuda_graph_of_device_dt_steps_equals_plain_loop(npackets):
+    # the steady-state step (the gather-mode fill launches nothing, dt and the
+    # advance read / write device memory only) captured once in a CUDA graph
+    # and replayed: bitwise the plain device-dt loop, clock included
+    import torch
+    from paper_2507_09337_b200 import hydro
+    g = H.make_grid(3, (16, 16, 16), (2, 2, 2), bc=((R, O), (P, P), (O, R)))
+    U0 = inp.random_field(g.N, seed=67)
+    pa = H.gpu_setup(g, U0, npackets)
+    ca, loga = hydro.run_device(pa, 8)
+    pb = H.gpu_setup(g, U0, npackets)
+    clock = hydro.DevClock()
+    for _ in range(2):  # steady state first (records from the fused epilogue; not captured)
+        hydro.orcha_fill_guardcells(pb)
+        hydro.orcha_compute_dt_device(pb, clock)
+        hydro.step_devdt(pb, clock.dt_tensor)
+    graph = hydro.capture_steps(pb, clock, 2)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(H.gather(g, pb), H.gather(g, pa))
+    cb = clock.read()
+    assert (cb.t, cb.dt, cb.argmax, cb.steps) == (ca.read().t, ca.read().dt, ca.read().argmax, 8)

@@ -43,6 +43,14 @@
 #ifndef ORCHA_CONV_SPLIT
 #define ORCHA_CONV_SPLIT 1
 #endif
+// face-task rounds per warp (16^3 / 32^3): stage 1 (and both per-stage
+// stages) / telescoped stage 2 (3: 5-warp CTAs, 3 per SM; measured best)
+#ifndef ORCHA_ROUNDS1
+#define ORCHA_ROUNDS1 2
+#endif
+#ifndef ORCHA_ROUNDS2
+#define ORCHA_ROUNDS2 3
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 #ifndef ORCHA_ISSUE_LAST
 #define ORCHA_ISSUE_LAST 0
@@ -108,7 +116,8 @@ struct Geo {
   // warp count is chosen so every warp gets two slots (two rounds)
   static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
   static constexpr int NSLOT = SX + SY + SZ;
-  static constexpr int NW = (NB >= 16) ? (NSLOT + 1) / 2 : (W * W + 31) / 32;
+  static constexpr int RQ = (STAGE == 1 || MODE == 1) ? ORCHA_ROUNDS1 : ORCHA_ROUNDS2;  // face rounds per warp and plane
+  static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ : (W * W + 31) / 32;
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
@@ -116,7 +125,9 @@ struct Geo {
       sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64 + ((NS * IR + 15) / 16) * 16;
   // CTAs per SM we aim for: shared memory bound (227 KB per SM), at most 4
   static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
-  static constexpr int MINB = MINB_S < 1 ? 1 : (MINB_S > 4 ? 4 : MINB_S);
+  static constexpr int MINB_R = 65536 / (NT * 80);  // at ~80 registers per thread
+  static constexpr int MINB_SR = MINB_S < MINB_R ? MINB_S : MINB_R;
+  static constexpr int MINB = MINB_SR < 1 ? 1 : (MINB_SR > 4 ? 4 : MINB_SR);
   static_assert(NT >= FZ, "one update cell per thread");
   static_assert((BAND * 8) % 16 == 0, "bulk copies need 16-byte multiples");
 };

@@ -192,19 +192,11 @@ def cpu_baseline(seconds_target=15.0):
 
 
 # ----------------------------------------------------------------- GPU arm
-def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_priority=0, copy_streams=2):
-    """End to end with a host-resident mesh (SURVEY 8(f) F3, the paper's
-    execution model: every cycle each DataPacket is shipped H2D, advanced and
-    shipped back, P:L497-502): the brick is K z-slab packets whose interiors
-    live in pinned host memory.  Per step: pack every packet (H2D stream;
-    packet i waits for its own D2H of the previous step) -> fill + dt over
-    the set -> advance packet i -> unpack it (D2H stream, no sync) while
-    packet i+1 is advanced.  Step n+1 consumes step n's output from the host
-    mesh: a real simulation loop, not independent replicas.  Timed with CUDA
-    events on the compute stream (max over ranks)."""
+def streamed_loop(g, ids, N, px, py, pz, comm, stream, K, copy_priority=0, copy_streams=2):
+    """The streamed time step of streamed_e2e: returns (packets, host mesh,
+    step function, per-packet D2H-done events)."""
     import numpy as np
     import torch
-    import torch.distributed as dist
 
     import orcha_inputs as inp
     from paper_2507_09337_b200 import hydro
@@ -260,7 +252,23 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
             e2 = torch.cuda.Event()
             e2.record(d2h)
             done[i] = e2
+    return pks, mesh, one, done
 
+
+def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_priority=0, copy_streams=2):
+    """End to end with a host-resident mesh (SURVEY 8(f) F3, the paper's
+    execution model: every cycle each DataPacket is shipped H2D, advanced and
+    shipped back, P:L497-502): the brick is K z-slab packets whose interiors
+    live in pinned host memory.  Per step: pack every packet (H2D stream;
+    packet i waits for its own D2H of the previous step) -> fill + dt over
+    the set -> advance packet i -> unpack it (D2H stream, no sync) while
+    packet i+1 is advanced.  Step n+1 consumes step n's output from the host
+    mesh: a real simulation loop, not independent replicas.  Timed with CUDA
+    events on the compute stream (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    pks, mesh, one, done = streamed_loop(g, ids, N, px, py, pz, comm, stream, K, copy_priority, copy_streams)
     one()
     torch.cuda.synchronize()
     if world > 1:
@@ -306,7 +314,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="orcha", choices=["orcha", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-priority", type=int, default=-1,
                     help="streamed e2e: CUDA priority of the copy streams (-1 = high)")
     ap.add_argument("--e2e-copy-streams", type=int, default=2,

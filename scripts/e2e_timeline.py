@@ -1,8 +1,8 @@
-"""Timeline of the streamed e2e step (bench.py streamed_e2e) from the CUDA
-activity trace of torch.profiler (CUPTI): per step, every memcpy and kernel
-with its start / end relative to the step's first H2D.  Diagnostic only."""
+"""Timeline of bench.py's streamed e2e step (bench.streamed_loop, the exact
+loop `e2e` times) from the CUDA activity trace of torch.profiler (CUPTI):
+every memcpy and kernel with its start / end, plus per-step link idle time.
+Diagnostic only.  Usage: python scripts/e2e_timeline.py [packets] [copy_streams]"""
 import json
-import math
 import sys
 
 import numpy as np
@@ -10,49 +10,19 @@ import torch
 
 sys.path.insert(0, ".")
 import bench  # noqa: E402
-import orcha_inputs as inp  # noqa: E402
 from paper_2507_09337_b200 import abi, hydro  # noqa: E402
 
 
-def main(K=8, nsteps=3, prio=-1):
+def main(K=16, cs=2, nsteps=3):
     torch.cuda.set_device(0)
     lib = abi.load(False)
     abi.call(lib, "orcha_set_fill_mode", 1)
     nblk = bench.BRICK_BLOCKS
-    NB = bench.NB
-    N = tuple(nblk[a] * NB[a] for a in range(3))
-    g = hydro.Grid(3, NB, nblk, xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0))
+    N = tuple(nblk[a] * bench.NB[a] for a in range(3))
+    g = hydro.Grid(3, bench.NB, nblk, xmin=(0.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0))
     ids = np.arange(nblk[0] * nblk[1] * nblk[2])
-    slabs = [a for a in np.array_split(ids, K) if len(a)]
-    pks = [hydro.Packet(g, a) for a in slabs]
-    mesh = [torch.from_numpy(inp.sedov_packet(N, NB, a, xmax=(1.0, 1.0, 1.0))).pin_memory() for a in slabs]
     stream = torch.cuda.current_stream()
-    h2d, d2h = torch.cuda.Stream(priority=prio), torch.cuda.Stream(priority=prio)
-    done = [None] * len(pks)
-
-    def one():
-        ev_in = []
-        for i, p in enumerate(pks):
-            if done[i] is not None:
-                h2d.wait_event(done[i])
-            p.pack(mesh[i], h2d)
-            e = torch.cuda.Event()
-            e.record(h2d)
-            ev_in.append(e)
-        for e in ev_in:
-            stream.wait_event(e)
-        hydro.orcha_fill_guardcells(pks, None, stream)
-        info = hydro.orcha_compute_dt(pks, math.inf, None, stream)
-        for i, p in enumerate(pks):
-            hydro.orcha_hydro_advance(p, info.dt, stream)
-            e = torch.cuda.Event()
-            e.record(stream)
-            d2h.wait_event(e)
-            p.unpack(mesh[i], d2h, sync=False)
-            e2 = torch.cuda.Event()
-            e2.record(d2h)
-            done[i] = e2
-
+    pks, mesh, one, done = bench.streamed_loop(g, ids, N, 1, 1, 1, None, stream, K, -1, cs)
     one()
     one()
     torch.cuda.synchronize()
@@ -71,8 +41,23 @@ def main(K=8, nsteps=3, prio=-1):
     out = [(round((s - t0) / 1e3, 3), round((e - t0) / 1e3, 3), n) for s, e, n in ev]
     for s, e, n in out:
         print(f"{s:9.3f} {e:9.3f} {e - s:7.3f}  {n}")
+    # per direction: busy time (union of copy intervals) over the whole trace
+    span = out[-1][1] - out[0][0]
+    for tag in ("HtoD", "DtoH"):
+        iv = sorted((s, e) for s, e, n in out if tag in n and "Pinned" in n)
+        busy, cur = 0.0, None
+        for s, e in iv:
+            if cur is None or s > cur[1]:
+                if cur:
+                    busy += cur[1] - cur[0]
+                cur = [s, e]
+            else:
+                cur[1] = max(cur[1], e)
+        if cur:
+            busy += cur[1] - cur[0]
+        print(f"# {tag}: busy {busy:.2f} of {span:.2f} ms ({100 * busy / span:.0f} %)")
     json.dump(out, open("gpurun_out/e2e_timeline.json", "w"))
 
 
 if __name__ == "__main__":
-    main(K=int(sys.argv[1]) if len(sys.argv) > 1 else 8)
+    main(K=int(sys.argv[1]) if len(sys.argv) > 1 else 16, cs=int(sys.argv[2]) if len(sys.argv) > 2 else 2)

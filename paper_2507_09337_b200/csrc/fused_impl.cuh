@@ -44,7 +44,8 @@
 #define ORCHA_CONV_SPLIT 1
 #endif
 // face-task rounds per warp (16^3 / 32^3): stage 1 (and both per-stage
-// stages) / telescoped stage 2 (3: 5-warp CTAs, 3 per SM; measured best)
+// stages, and 32^3 blocks) / telescoped 16^3 stage 2 (3: 5-warp CTAs, 3 per
+// SM; measured best -- 32^3 stage 2 is faster with 2: 5.57 vs 5.36 G)
 #ifndef ORCHA_ROUNDS1
 #define ORCHA_ROUNDS1 2
 #endif
@@ -116,7 +117,7 @@ struct Geo {
   // warp count is chosen so every warp gets two slots (two rounds)
   static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
   static constexpr int NSLOT = SX + SY + SZ;
-  static constexpr int RQ = (STAGE == 1 || MODE == 1) ? ORCHA_ROUNDS1 : ORCHA_ROUNDS2;  // face rounds per warp and plane
+  static constexpr int RQ = (STAGE == 1 || MODE == 1 || NB != 16) ? ORCHA_ROUNDS1 : ORCHA_ROUNDS2;  // face rounds per warp and plane
   static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ : (W * W + 31) / 32;
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;

@@ -52,6 +52,10 @@
 #ifndef ORCHA_ROUNDS2
 #define ORCHA_ROUNDS2 3
 #endif
+// 8^3 blocks: face rounds per warp (0: one warp per 32 cells of the plane)
+#ifndef ORCHA_ROUNDS8
+#define ORCHA_ROUNDS8 0
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 #ifndef ORCHA_ISSUE_LAST
 #define ORCHA_ISSUE_LAST 0
@@ -118,7 +122,10 @@ struct Geo {
   static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
   static constexpr int NSLOT = SX + SY + SZ;
   static constexpr int RQ = (STAGE == 1 || MODE == 1 || NB != 16) ? ORCHA_ROUNDS1 : ORCHA_ROUNDS2;  // face rounds per warp and plane
-  static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ : (W * W + 31) / 32;
+  static constexpr int NW8 = (NSLOT + ORCHA_ROUNDS8 - 1) / (ORCHA_ROUNDS8 > 0 ? ORCHA_ROUNDS8 : 1);
+  static constexpr int NWU = (FZ + 31) / 32;                 // one update cell per thread
+  static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ
+                                       : (ORCHA_ROUNDS8 > 0 ? (NW8 > NWU ? NW8 : NWU) : (W * W + 31) / 32);
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
@@ -128,7 +135,7 @@ struct Geo {
   static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
   static constexpr int MINB_R = 65536 / (NT * 80);  // at ~80 registers per thread
   static constexpr int MINB_SR = MINB_S < MINB_R ? MINB_S : MINB_R;
-  static constexpr int MINB = MINB_SR < 1 ? 1 : (MINB_SR > 4 ? 4 : MINB_SR);
+  static constexpr int MINB = MINB_SR < 1 ? 1 : (MINB_SR > 8 ? 8 : MINB_SR);
   static_assert(NT >= FZ, "one update cell per thread");
   static_assert((BAND * 8) % 16 == 0, "bulk copies need 16-byte multiples");
 };

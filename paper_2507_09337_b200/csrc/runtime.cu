@@ -837,6 +837,22 @@ extern "C" int32_t orcha_fill_guardcells_stage(orcha_packet* const* pk, int32_t 
 }
 
 // --------------------------------------------------------------- dt ------
+// The per-packet CFL records of every packet whose records are stale (after a
+// pack); an advance leaves valid ones (the fused stage-2 epilogue).
+static int32_t ensure_dt_records(orcha_packet* const* pk, int32_t npk, cudaStream_t s) {
+  for (int q = 0; q < npk; q++) {
+    orcha_packet* p = pk[q];
+    if (!p) return fail(ORCHA_E_ARG, "null packet");
+    if (!p->records_valid) {
+      cudaError_t e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords,
+                                p->status, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dt kernel");
+      p->records_valid = true;
+    }
+  }
+  return ORCHA_OK;
+}
+
 extern "C" int32_t orcha_packet_dt_records(orcha_packet* p, void* stream) {
   if (!p) return fail(ORCHA_E_ARG, "null packet");
   cudaError_t e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords, p->status,
@@ -852,15 +868,9 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<DtRecord> res(npk);
   std::vector<DevStatus> st(npk);
-  for (int q = 0; q < npk; q++) {
-    orcha_packet* p = pk[q];
-    if (!p) return fail(ORCHA_E_ARG, "null packet");
-    if (!p->records_valid) {
-      cudaError_t e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords,
-                                p->status, s);
-      if (e != cudaSuccess) return cuda_fail(e, "dt kernel");
-      p->records_valid = true;
-    }
+  {
+    int32_t rc = ensure_dt_records(pk, npk, s);
+    if (rc) return rc;
   }
   if (npk > 1) {
     // one reduction over every packet's records and status word (the same
@@ -919,15 +929,9 @@ extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk,
                                            orcha_dev_clock* d_clock, void* stream) {
   if (!pk || npk < 1 || !d_clock) return fail(ORCHA_E_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  for (int q = 0; q < npk; q++) {
-    orcha_packet* p = pk[q];
-    if (!p) return fail(ORCHA_E_ARG, "null packet");
-    if (!p->records_valid) {
-      cudaError_t e = launch_dt(p->grid->dev, p->state, p->nslots, p->d_slots, p->records, &p->nrecords,
-                                p->status, s);
-      if (e != cudaSuccess) return cuda_fail(e, "dt kernel");
-      p->records_valid = true;
-    }
+  {
+    int32_t rc = ensure_dt_records(pk, npk, s);
+    if (rc) return rc;
   }
   const DtRecord* r = nullptr;
   const DevStatus* st = nullptr;

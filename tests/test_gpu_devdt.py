@@ -124,3 +124,18 @@ def test_cuda_graph_of_device_dt_steps_equals_plain_loop(npackets):
     assert np.array_equal(H.gather(g, pb), H.gather(g, pa))
     cb = clock.read()
     assert (cb.t, cb.dt, cb.argmax, cb.steps) == (ca.read().t, ca.read().dt, ca.read().argmax, 8)
+
+
+@pytest.mark.parametrize("scheme", [dict(riemann=1), dict(limiter=1), dict(eos=1, arad=1e-4)])
+def test_device_dt_loop_with_scheme_variants(scheme):
+    # the device clock with the F4 variants (HLLC, MC, the gas + radiation EOS,
+    # whose dt uses Gamma_1): bitwise the host-dt loop, parity build against
+    # the oracle as well
+    g = H.make_grid(3, (8, 8, 8), (2, 2, 2), bc=((O, O), (P, P), (R, O)), parity=True, **scheme)
+    U0 = inp.sedov(g.N)
+    (A, ta, loga), (B, c, logb) = _both(g, U0, 3)
+    assert logb == [tuple(x) for x in loga]
+    assert np.array_equal(A, B)
+    O_, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=3)
+    assert [x[0] for x in logb] == olog.dts
+    assert np.array_equal(B, O_)

@@ -60,6 +60,13 @@
 #ifndef ORCHA_EXTRA_WARPS2
 #define ORCHA_EXTRA_WARPS2 0
 #endif
+// the same for the per-stage (F1) kernels and for 32^3 blocks
+#ifndef ORCHA_EXTRA_WARPS_PS
+#define ORCHA_EXTRA_WARPS_PS 0
+#endif
+#ifndef ORCHA_EXTRA_WARPS32
+#define ORCHA_EXTRA_WARPS32 2
+#endif
 // 8^3 blocks: face rounds per warp (0: one warp per 32 cells of the plane)
 #ifndef ORCHA_ROUNDS8
 #define ORCHA_ROUNDS8 0
@@ -132,7 +139,10 @@ struct Geo {
   static constexpr int RQ = (STAGE == 1 || MODE == 1 || NB != 16) ? ORCHA_ROUNDS1 : ORCHA_ROUNDS2;  // face rounds per warp and plane
   static constexpr int NW8 = (NSLOT + ORCHA_ROUNDS8 - 1) / (ORCHA_ROUNDS8 > 0 ? ORCHA_ROUNDS8 : 1);
   static constexpr int NWU = (FZ + 31) / 32;                 // one update cell per thread
-  static constexpr int XW = (NB != 16 || MODE != 0) ? 0 : (STAGE == 1 ? ORCHA_EXTRA_WARPS1 : ORCHA_EXTRA_WARPS2);
+  static constexpr int XW = NB == 32 ? ORCHA_EXTRA_WARPS32
+                            : NB != 16 ? 0
+                            : MODE == 1 ? ORCHA_EXTRA_WARPS_PS
+                                        : (STAGE == 1 ? ORCHA_EXTRA_WARPS1 : ORCHA_EXTRA_WARPS2);
   static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ + XW
                                        : (ORCHA_ROUNDS8 > 0 ? (NW8 > NWU ? NW8 : NWU) : (W * W + 31) / 32);
   static constexpr int NT = NW * 32;

@@ -67,6 +67,12 @@
 #ifndef ORCHA_EXTRA_WARPS32
 #define ORCHA_EXTRA_WARPS32 2
 #endif
+#ifndef ORCHA_EXTRA_WARPS8_1
+#define ORCHA_EXTRA_WARPS8_1 0
+#endif
+#ifndef ORCHA_EXTRA_WARPS8_2
+#define ORCHA_EXTRA_WARPS8_2 2
+#endif
 // 8^3 blocks: face rounds per warp (0: one warp per 32 cells of the plane)
 #ifndef ORCHA_ROUNDS8
 #define ORCHA_ROUNDS8 0
@@ -144,7 +150,8 @@ struct Geo {
                             : MODE == 1 ? ORCHA_EXTRA_WARPS_PS
                                         : (STAGE == 1 ? ORCHA_EXTRA_WARPS1 : ORCHA_EXTRA_WARPS2);
   static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ + XW
-                                       : (ORCHA_ROUNDS8 > 0 ? (NW8 > NWU ? NW8 : NWU) : (W * W + 31) / 32);
+                                       : (ORCHA_ROUNDS8 > 0 ? (NW8 > NWU ? NW8 : NWU) : (W * W + 31) / 32) +
+                                             (STAGE == 2 ? ORCHA_EXTRA_WARPS8_2 : ORCHA_EXTRA_WARPS8_1);
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)

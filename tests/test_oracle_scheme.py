@@ -38,15 +38,130 @@ def test_cfg1_matches_independent_prototype():
     assert log.floor_hits == gold["floor_hits"]
 
 
+def sedov_energy_closed_form(N):
+    """E_blast + (N_cells - n_D) dV p_amb/(gamma-1) (SURVEY 8(c) "Initial conditions")."""
+    nd = len(N)
+    dV = 1.0
+    ncell = 1
+    for n in N:
+        dV = dV / n
+        ncell *= n
+    return 1.0 + (ncell - inp.sedov_deposit_count(nd)) * dV * 1e-5 / 0.4
+
+
 @pytest.mark.slow
 def test_cfg3_matches_independent_prototype():
+    # BASELINE configs[2] (128^3, 10 steps) against the survey-time numpy
+    # prototype.  Its sums ran in numpy's pairwise order, the oracle's here in
+    # np.sum's order over a different array view, so sum E (a 2M-term sum of
+    # values ~1e-5 and ~1e3) agrees to a few ulp, not bitwise: the closed-form
+    # initial energy (the blast has not reached the outflow walls, so E is
+    # conserved) is the exact pin, the prototype value a 1e-14 cross-check.
     gold = json.load(open(os.path.join(GOLD, "sedov3d_cfg3.json")))
     g = oracle.Grid(N=tuple(gold["N"]))
     I, log = run_fresh(g, inp.sedov(g.N), nsteps=gold["steps"])
     assert abs(log.dts[0] - gold["dt0"]) <= 1e-15 * gold["dt0"]
     assert log.t == gold["t10"]
     assert abs(I[0].max() - gold["max_rho"]) <= 1e-15 * gold["max_rho"]
-    assert I[4].sum() / 128 ** 3 == gold["sum_E_dV"]
+    sumE = I[4].sum() / 128 ** 3
+    assert abs(sumE - sedov_energy_closed_form(g.N)) <= 1e-15
+    assert abs(sumE - gold["sum_E_dV"]) <= 1e-14
+    assert abs(I[0].sum() / 128 ** 3 - 1.0) <= 1e-15
+
+
+def _shell_radius(rho, dx):
+    """Radius of the peak of the shell-averaged density (cells binned by
+    floor(r/dx) about the centre vertex)."""
+    n = rho.shape[-1]
+    xc = (np.arange(n) + 0.5) * dx - 0.5
+    r2 = xc[None, None, :] ** 2 + xc[None, :, None] ** 2 + xc[:, None, None] ** 2
+    b = (np.sqrt(r2) / dx).astype(int).ravel()
+    mean = np.bincount(b, rho.ravel()) / np.bincount(b)
+    return (np.argmax(mean) + 0.5) * dx
+
+
+@pytest.mark.parametrize("N", [32, pytest.param(64, marks=pytest.mark.slow)])
+def test_sedov_3d_shock_radius(N):
+    # P:L591-593 (sec 5.2): "an analytical expression exists for how far the
+    # shock has traveled"; north_star: r = xi0 (E t^2/rho)^(1/5) in 3D with
+    # xi0 = 1.032777 (gamma = 1.4, tests/exact/sedov.py).  Gate |R - R_th| <=
+    # 2 dx at t = 0.05 (R_th = 0.3116).  Mass and energy are conserved to
+    # round-off while the shock is inside the box.
+    g = oracle.Grid(N=(N, N, N))
+    I, log = run_fresh(g, inp.sedov(g.N), t_end=0.05)
+    dx = 1.0 / N
+    Rth = sedov.shock_radius(0.05, 3)
+    assert abs(sedov.xi0(3) - 1.032777) < 2e-6
+    assert abs(Rth - 0.31160) < 1e-5
+    R = _shell_radius(I[0], dx)
+    assert abs(R - Rth) <= 2 * dx, (R, Rth, dx)
+    assert log.t == 0.05 and log.tags[-1] == oracle.TAG_CLAMP
+    assert abs(I[0].sum() * dx ** 3 - 1.0) <= 1e-14
+    assert abs(I[4].sum() * dx ** 3 - sedov_energy_closed_form(g.N)) <= 1e-14
+    assert log.floor_hits == 0
+
+
+def _advance_prescribed(g, U0, dts):
+    """Advance with a given dt sequence (ghost fill + one RK2 step each)."""
+    U = oracle.padded(g, U0)
+    for dt in dts:
+        oracle.fill_ghosts(g, U)
+        rc, _ = oracle.step(g, U, dt)
+        assert rc == 0
+    return U[g.interior].copy()
+
+
+def test_noncubic_cells_tube_along_y_equals_1d_run():
+    # The flux divergence's per-axis 1/dx (SURVEY 8(a) A8): a Sod tube along y
+    # on cells with dx != dy (x periodic, so every x-face flux difference is
+    # exactly 0) must advance exactly like the 1D tube with spacing dy, given
+    # the same dt sequence.  Multiplying dF_y by 1/dx (or the wrong axis'
+    # spacing anywhere) changes every cell.
+    N = 64
+    d1 = oracle.Grid(N=(N,))
+    X, log = run_fresh(d1, inp.sod(d1.N), nsteps=25)
+    nx = 6
+    g2 = oracle.Grid(N=(nx, N), xmax=(0.37, 1.0), bc=((P, P), (O, O), (O, O)))
+    Y = _advance_prescribed(g2, inp.sod(g2.N, axis=1), log.dts)
+    for i in range(nx):
+        col = Y[:, 0, :, i]
+        assert np.array_equal(col[0], X[0, 0, 0])
+        assert np.array_equal(col[2], X[1, 0, 0])      # normal momentum
+        assert np.array_equal(col[4], X[4, 0, 0])
+        assert np.all(col[1] == 0.0) and np.all(col[3] == 0.0)
+
+
+def test_noncubic_cells_tube_along_z_equals_1d_run():
+    # the same along z with three different spacings (dz = 1/48)
+    N = 48
+    d1 = oracle.Grid(N=(N,))
+    X, log = run_fresh(d1, inp.sod(d1.N), nsteps=20)
+    g3 = oracle.Grid(N=(4, 6, N), xmax=(0.29, 0.53, 1.0), bc=((P, P), (P, P), (O, O)))
+    Z = _advance_prescribed(g3, inp.sod(g3.N, axis=2), log.dts)
+    for j in range(6):
+        for i in range(4):
+            assert np.array_equal(Z[0, :, j, i], X[0, 0, 0])
+            assert np.array_equal(Z[3, :, j, i], X[1, 0, 0])
+            assert np.array_equal(Z[4, :, j, i], X[4, 0, 0])
+    assert np.all(Z[1] == 0.0) and np.all(Z[2] == 0.0)
+
+
+def test_noncubic_cells_cfl_closed_form():
+    # A4 on a uniform moving state with three different spacings and three
+    # different speeds: dt = cfl / sum_d (|v_d| + c)/dx_d, c = sqrt(gamma p/rho).
+    # Pairing a speed with the wrong spacing moves dt by > 10 %.
+    g = oracle.Grid(N=(8, 10, 12), xmax=(0.5, 2.0, 0.3), bc=((P, P),) * 3)
+    rho, vel, p = 1.7, (0.9, -2.3, 0.4), 0.6
+    U = oracle.padded(g, inp.uniform(g.N, rho, vel, p))
+    oracle.fill_ghosts(g, U)
+    r = oracle.compute_dt(g, U)
+    c = np.sqrt(1.4 * p / rho)
+    dxs = (0.5 / 8, 2.0 / 10, 0.3 / 12)
+    expect = 0.4 / sum((abs(v) + c) / h for v, h in zip(vel, dxs))
+    assert abs(r.dt - expect) <= 4e-16 * expect
+    perm = 0.4 / sum((abs(v) + c) / h for v, h in zip(vel, dxs[::-1]))
+    assert abs(perm - expect) > 0.1 * expect
+    assert r.argmax == 0 and r.tag == oracle.TAG_CFL
 
 
 @pytest.mark.parametrize("nd", [2, 3])

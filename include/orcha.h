@@ -356,6 +356,32 @@ int32_t orcha_set_guard_push(int32_t on);
 
 const char* orcha_last_error(void);
 
+/* ------------------------------------------------ unit entry points ----- */
+/* The per-cell / per-face device functions the fused kernels call, applied to
+ * n independent inputs (test diagnostics for SURVEY 8(d)'s unit fuzz; the hot
+ * path never calls these).  The scheme is the grid's: with no F4 flag set the
+ * paper-path functions (A5 gamma-law EOS, A6 minmod PLM, A7 HLL -- in the
+ * production build its expanded algebra), otherwise the F4 variants.  All
+ * buffers are caller-owned DEVICE memory, variable-major with stride n
+ * (element v of item i at [v*n + i]); n in [0, 2^31/5].  Asynchronous on
+ * `stream`.  Errors: ORCHA_E_ARG (null grid/buffer, n or dir out of range),
+ * ORCHA_E_CUDA.
+ *
+ * orcha_unit_eos: conserved d_U[5][n] -> primitives d_Q[5][n] (rho, u, v, w,
+ *   p after the floor), sound speed d_c[n], 3D CFL signal-speed sum d_s[n]
+ *   (A4's s with the grid's 1/dx), floor flag d_floored[n] (A5, c10).
+ * orcha_unit_face_flux: primitives of the 4-cell stencil d_q[4][5][n]
+ *   (cells i-1, i, i+1, i+2 along dir) -> flux through face i+1/2, d_F[5][n]
+ *   (A6 + A7).
+ * orcha_unit_riemann: face states d_qL[5][n], d_qR[5][n] (primitives) ->
+ *   Riemann flux along dir, d_F[5][n] (A7; HLLC reading c20 with the flag). */
+int32_t orcha_unit_eos(const orcha_grid* grid, int64_t n, const double* d_U, double* d_Q, double* d_c,
+                       double* d_s, int32_t* d_floored, void* stream);
+int32_t orcha_unit_face_flux(const orcha_grid* grid, int32_t dir, int64_t n, const double* d_q, double* d_F,
+                             void* stream);
+int32_t orcha_unit_riemann(const orcha_grid* grid, int32_t dir, int64_t n, const double* d_qL,
+                           const double* d_qR, double* d_F, void* stream);
+
 /* ------------------------------------------------------- multi-GPU ------ */
 
 /* Communicator for blocks partitioned over ranks (one process per GPU,
@@ -381,6 +407,15 @@ int32_t orcha_comm_create_local(const orcha_grid* grid, int32_t nranks, const in
                                 orcha_comm** out);
 int32_t orcha_comm_push(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, int32_t buffer,
                         void* stream);  /* buffer: 0 = state, 1 = stage-1 buffer */
+/* LOCAL transport, dt: pushes this virtual rank's 32-byte dt record (max
+ * signal speed s over its packets, lowest global cell index g, non-physical
+ * flag -- what the NCCL path allgathers) into slot `rank` of every member's
+ * gather buffer.  Call it for EVERY virtual rank (after the step's fill),
+ * then orcha_compute_dt / orcha_compute_dt_device for each with its own
+ * communicator: each reduces all ranks' records with the single-GPU rule
+ * (max s, ties -> lowest g, NaN wins), exactly as after an ncclAllGather.
+ * Errors: ORCHA_E_ARG (NCCL communicator, null argument), ORCHA_E_CUDA. */
+int32_t orcha_comm_push_dt(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, void* stream);
 
 /* Host-only view of the guard exchange plan between `rank` and `peer` (no
  * device work; for tests and tooling).  The plan is a pure function of the

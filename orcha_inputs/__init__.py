@@ -184,6 +184,40 @@ def random_field(N: Sequence[int], seed: int = SEED, amp: float = 0.3,
     return U
 
 
+def supersonic_field(N: Sequence[int], seed: int = SEED, mach: float = 2.5, amp: float = 0.2,
+                     gamma: float = 1.4) -> np.ndarray:
+    """Rough field with supersonic shear flow along every active axis, for the
+    HLL / HLLC one-sided branches (S_L >= 0, S_R <= 0): velocity component d
+    is +mach*c0 on one half of the domain along the next axis and -mach*c0 on
+    the other half (c0 = sqrt(gamma) at rho = p = 1), plus amp-sized noise in
+    rho, p and every velocity.  Along its own axis each component is smooth,
+    so the flow stays supersonic there without shocks."""
+    Nx, Ny, Nz = _dims(N)
+    nd = len(N)
+    rng = np.random.default_rng(seed)
+    shp = (Nz, Ny, Nx)
+    c0 = np.sqrt(gamma)
+    rho = 1.0 + amp * rng.uniform(-1.0, 1.0, shp)
+    p = 1.0 + amp * rng.uniform(-1.0, 1.0, shp)
+    idx = np.indices(shp)                     # (k, j, i)
+    ext = (Nx, Ny, Nz)
+    vel = []
+    for d in range(3):
+        if d >= nd:
+            vel.append(np.zeros(shp))
+            continue
+        e = (d + 1) % nd                      # the axis the sign flips along
+        half = idx[2 - e] < ext[e] // 2
+        sign = np.where(half, 1.0, -1.0) if nd > 1 else np.ones(shp)
+        vel.append(mach * c0 * sign + amp * rng.uniform(-1.0, 1.0, shp))
+    U = np.zeros((5,) + shp, dtype=np.float64)
+    U[0] = rho
+    for d in range(3):
+        U[1 + d] = rho * vel[d]
+    U[4] = p * (1.0 / (gamma - 1.0)) + 0.5 * rho * ((vel[0] * vel[0] + vel[1] * vel[1]) + vel[2] * vel[2])
+    return U
+
+
 def to_blocks(U: np.ndarray, nb: Sequence[int], block_ids: Sequence[int]) -> np.ndarray:
     """Global interior (5, Nz, Ny, Nx) -> packet interior (nblocks, 5, nbz, nby, nbx)
     for the given global block ids b = (bk*NBy + bj)*NBx + bi."""

@@ -31,7 +31,8 @@ EXPORTS = [
     "orcha_comm_create_local", "orcha_comm_push", "orcha_comm_plan", "orcha_hydro_stage",
     "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push", "orcha_set_fill_mode",
     "orcha_packet_unpack_async", "orcha_fill_guardcells_packet", "orcha_packet_dt_records",
-    "orcha_compute_dt_device",
+    "orcha_compute_dt_device", "orcha_unit_eos", "orcha_unit_face_flux", "orcha_unit_riemann",
+    "orcha_comm_push_dt",
 ]
 
 
@@ -131,6 +132,10 @@ _SIGS = {
     "orcha_hydro_stage_devdt": (_i32, [_vp, _i32, _vp, _vp]),
     "orcha_fill_guardcells_stage": (_i32, [_P(_vp), _i32, _vp, _i32, _vp]),
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),
+    "orcha_comm_push_dt": (_i32, [_vp, _P(_vp), _i32, _vp]),
+    "orcha_unit_eos": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "orcha_unit_face_flux": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),
+    "orcha_unit_riemann": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp, _vp]),
 }
 
 _loaded = {}

@@ -244,8 +244,15 @@ struct CommPlan {
   long long n_unpack = 0;
 };
 
+// Virtual ranks sharing one device: members[r] is virtual rank r (nullptr
+// once destroyed; the hub goes when every slot is empty).
 struct Hub {
   std::vector<orcha_comm*> members;
+  bool empty() const {
+    for (auto* m : members)
+      if (m) return false;
+    return true;
+  }
 };
 
 }  // namespace orcha
@@ -392,6 +399,7 @@ static int32_t pack_all(orcha_comm* c, CommPlan* P, bool into_peers, cudaStream_
     double* dst = c->bufs[i].d_send;
     if (into_peers) {
       orcha_comm* peer = c->hub->members[c->bufs[i].peer];
+      if (!peer) return fail(ORCHA_E_STATE, "LOCAL peer rank was destroyed");
       dst = nullptr;
       for (auto& b : peer->bufs)
         if (b.peer == c->rank) dst = b.d_recv;
@@ -429,14 +437,36 @@ int32_t comm_exchange(orcha_comm* c, CommPlan* P, cudaStream_t s) {
   return unpack_all(c, P, s);
 }
 
+// The allgather of the 32-byte per-rank records into d_gather + 32 (slot r
+// = rank r), from this rank's record at `mine` (device).  NCCL: one
+// ncclAllGather.  LOCAL: every virtual rank pushed its record into every
+// member's slot beforehand (orcha_comm_push_dt); only the own slot is
+// (re)written here -- the same array the NCCL path produces.
+static int32_t gather_records(orcha_comm* c, const void* mine, cudaStream_t s) {
+  char* base = (char*)c->d_gather;
+  cudaError_t e = cudaSuccess;
+  if (mine != base) e = cudaMemcpyAsync(base, mine, 32, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "dt record copy");
+  if (c->local) {
+    e = cudaMemcpyAsync(base + 32 + 32 * (size_t)c->rank, base, 32, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt record copy (LOCAL)");
+    return ORCHA_OK;
+  }
+  ncclResult_t r = nccl().AllGather(base, base + 32, 32, ncclUint8, c->nc, s);
+  if (r != ncclSuccess) return nccl_fail(r, "dt allgather");
+  return ORCHA_OK;
+}
+
+// Host-result dt: this rank's (smax, g, bad) -> the global one by the
+// single-GPU rule (max s, ties -> lowest g, NaN wins) over all ranks' records.
 int32_t comm_allreduce_dt(orcha_comm* c, double* smax, long long* g, bool* bad, cudaStream_t s) {
-  if (c->local || c->nranks == 1) return ORCHA_OK;  // LOCAL: the caller reduces over all virtual ranks
+  if (c->nranks == 1 && !c->local) return ORCHA_OK;
   GatherRec mine{*smax, *g, *bad ? 1 : 0, 0};
   char* base = (char*)c->d_gather;
   cudaError_t e = cudaMemcpyAsync(base, &mine, sizeof mine, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "dt gather upload");
-  ncclResult_t r = nccl().AllGather(base, base + 32, 32, ncclUint8, c->nc, s);
-  if (r != ncclSuccess) return nccl_fail(r, "dt allgather");
+  int32_t rc = gather_records(c, base, s);
+  if (rc) return rc;
   std::vector<GatherRec> all(c->nranks);
   e = cudaMemcpyAsync(all.data(), base + 32, 32 * (size_t)c->nranks, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -458,18 +488,30 @@ int32_t comm_allreduce_dt(orcha_comm* c, double* smax, long long* g, bool* bad, 
 // the communicator's buffer, no host round trip; returns the gathered array.
 int32_t comm_allgather_dt_device(orcha_comm* c, const GatherRec* mine, const GatherRec** all, int* nall,
                                  cudaStream_t s) {
-  if (c->local) return fail(ORCHA_E_ARG, "orcha_compute_dt_device: LOCAL (virtual-rank) communicators are not supported");
   char* base = (char*)c->d_gather;
-  cudaError_t e = cudaMemcpyAsync(base, mine, 32, cudaMemcpyDeviceToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "dt record copy");
-  if (c->nranks > 1) {
-    ncclResult_t r = nccl().AllGather(base, base + 32, 32, ncclUint8, c->nc, s);
-    if (r != ncclSuccess) return nccl_fail(r, "dt allgather");
-    *all = (const GatherRec*)(base + 32);
-    *nall = c->nranks;
-  } else {
+  if (c->nranks == 1 && !c->local) {
+    cudaError_t e = cudaMemcpyAsync(base, mine, 32, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt record copy");
     *all = (const GatherRec*)base;
     *nall = 1;
+    return ORCHA_OK;
+  }
+  int32_t rc = gather_records(c, mine, s);
+  if (rc) return rc;
+  *all = (const GatherRec*)(base + 32);
+  *nall = c->nranks;
+  return ORCHA_OK;
+}
+
+// LOCAL transport: this virtual rank's record (device) into slot `rank` of
+// every live member's gather buffer (the allgather, emulated by pushes).
+int32_t comm_push_dt_record(orcha_comm* c, const GatherRec* mine, cudaStream_t s) {
+  if (!c->local) return fail(ORCHA_E_ARG, "orcha_comm_push_dt is for LOCAL communicators only");
+  for (auto* m : c->hub->members) {
+    if (!m) continue;
+    cudaError_t e = cudaMemcpyAsync((char*)m->d_gather + 32 + 32 * (size_t)c->rank, mine, 32,
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt record push");
   }
   return ORCHA_OK;
 }
@@ -531,6 +573,7 @@ extern "C" int32_t orcha_comm_create_local(const orcha_grid* g, int32_t nranks, 
   int32_t rc = validate_owner(g, nranks, owner);
   if (rc) return rc;
   Hub* hub = new Hub();
+  hub->members.assign(nranks, nullptr);
   for (int r = 0; r < nranks; r++) {
     orcha_comm* c = new orcha_comm();
     c->grid = g;
@@ -542,11 +585,12 @@ extern "C" int32_t orcha_comm_create_local(const orcha_grid* g, int32_t nranks, 
     rc = setup_lists(c);
     if (rc) {
       destroy_comm(c);
-      for (auto* m : hub->members) destroy_comm(m);
+      for (auto* m : hub->members)
+        if (m) destroy_comm(m);
       delete hub;
       return rc;
     }
-    hub->members.push_back(c);
+    hub->members[r] = c;
   }
   std::lock_guard<std::mutex> lk(g_comm_mu);
   for (int r = 0; r < nranks; r++) {
@@ -573,9 +617,10 @@ extern "C" int32_t orcha_comm_destroy(orcha_comm* c) {
   g_comms.erase(std::remove(g_comms.begin(), g_comms.end(), c), g_comms.end());
   Hub* hub = c->hub;
   if (hub) {
-    hub->members.erase(std::remove(hub->members.begin(), hub->members.end(), c), hub->members.end());
-    // keep the hub alive while members remain (their pushes read peers' buffers)
-    if (hub->members.empty()) delete hub;
+    // the slot stays (members are indexed by rank); pushes to it now fail
+    for (auto*& m : hub->members)
+      if (m == c) m = nullptr;
+    if (hub->empty()) delete hub;
   }
   destroy_comm(c);
   return ORCHA_OK;

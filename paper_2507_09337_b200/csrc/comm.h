@@ -15,4 +15,10 @@ void comm_drop_packet(orcha_packet* p);
 int32_t comm_exchange(orcha_comm* comm, CommPlan* plan, cudaStream_t s);
 // Global (smax, argmax) with the lowest-g tie-break and the non-physical flag.
 int32_t comm_allreduce_dt(orcha_comm* comm, double* smax, long long* g, bool* bad, cudaStream_t s);
+// Device-resident dt: allgather this rank's record; *all / *nall = the
+// gathered records (every rank's, in rank order).
+int32_t comm_allgather_dt_device(orcha_comm* comm, const GatherRec* mine, const GatherRec** all, int* nall,
+                                 cudaStream_t s);
+// LOCAL transport: push this virtual rank's record to every member.
+int32_t comm_push_dt_record(orcha_comm* comm, const GatherRec* mine, cudaStream_t s);
 }  // namespace orcha

@@ -201,21 +201,6 @@ __device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, i
   }
 }
 
-// PLM + Riemann flux of one face.  SCH 0: the paper-path scheme (minmod +
-// HLL); SCH 1: the grid's F4 flags (limiter, Riemann solver) read at run time.
-template <int D, int SCH>
-__device__ __forceinline__ void face_flux(const Prim& q0, const Prim& q1, const Prim& q2, const Prim& q3,
-                                          const DevGrid& G, double* out, int stride) {
-  Prim L, R;
-  if constexpr (SCH == 0) {
-    plm_face(q0, q1, q2, q3, &L, &R);
-    hll_store<D>(L, R, G, out, stride);
-  } else {
-    plm_face_var(q0, q1, q2, q3, G, &L, &R);
-    flux_store_var<D>(L, R, G, out, stride);
-  }
-}
-
 // PUSH: 0 none, 1 scatter the new state into every same-packet guard
 // (push_cell), 2 into the x-guards only (push_x, gather mode).
 // GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a

@@ -920,15 +920,9 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
   return ORCHA_OK;
 }
 
-namespace orcha {
-int32_t comm_allgather_dt_device(orcha_comm* c, const GatherRec* mine, const GatherRec** all, int* nall,
-                                 cudaStream_t s);
-}
-
-extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
-                                           orcha_dev_clock* d_clock, void* stream) {
-  if (!pk || npk < 1 || !d_clock) return fail(ORCHA_E_ARG, "null argument");
-  cudaStream_t s = (cudaStream_t)stream;
+// This rank's dt record (device GatherRec: max s over its packets' records,
+// lowest g, non-physical flag) -- what the allgather carries.
+static int32_t rank_record(orcha_packet* const* pk, int32_t npk, cudaStream_t s, GatherRec** out) {
   {
     int32_t rc = ensure_dt_records(pk, npk, s);
     if (rc) return rc;
@@ -956,15 +950,35 @@ extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk,
   }
   e = launch_dt_gather_rec(r, st, mine, s);
   if (e != cudaSuccess) return cuda_fail(e, "dt record");
+  *out = mine;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
+                                           orcha_dev_clock* d_clock, void* stream) {
+  if (!pk || npk < 1 || !d_clock) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  GatherRec* mine = nullptr;
+  int32_t rc = rank_record(pk, npk, s, &mine);
+  if (rc) return rc;
   const GatherRec* all = mine;
   int nall = 1;
   if (comm) {
-    int32_t rc = comm_allgather_dt_device(comm, mine, &all, &nall, s);
+    rc = comm_allgather_dt_device(comm, mine, &all, &nall, s);
     if (rc) return rc;
   }
-  e = launch_dt_finish(all, nall, pk[0]->grid->dev.cfl, d_clock, s);
+  cudaError_t e = launch_dt_finish(all, nall, pk[0]->grid->dev.cfl, d_clock, s);
   if (e != cudaSuccess) return cuda_fail(e, "dt finish");
   return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_comm_push_dt(orcha_comm* comm, orcha_packet* const* pk, int32_t npk, void* stream) {
+  if (!comm || !pk || npk < 1) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  GatherRec* mine = nullptr;
+  int32_t rc = rank_record(pk, npk, s, &mine);
+  if (rc) return rc;
+  return comm_push_dt_record(comm, mine, s);
 }
 
 // ----------------------------------------------------------- advance -----

@@ -194,6 +194,11 @@ class Comm:
         arr, n = _handles(packets)
         abi.call(self.lib, "orcha_comm_push", self.handle, arr, n, int(buffer), ctypes.c_void_p(_stream_ptr(stream)))
 
+    def push_dt(self, packets, stream=None):
+        """LOCAL transport: publish this virtual rank's dt record to every member."""
+        arr, n = _handles(packets)
+        abi.call(self.lib, "orcha_comm_push_dt", self.handle, arr, n, ctypes.c_void_p(_stream_ptr(stream)))
+
     def destroy(self):
         if self.handle:
             self.lib.orcha_comm_destroy(self.handle)
@@ -409,3 +414,45 @@ def capture_steps(packets, clock: DevClock, nsteps: int, comm=None, method: str 
             step_devdt(packets, clock.dt_tensor, None, side, method)
     torch.cuda.current_stream().wait_stream(side)
     return g
+
+
+# ---- unit entry points (test diagnostics; include/orcha.h "unit entry points")
+def _dev_f64(a) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def orcha_unit_eos(grid: Grid, U: np.ndarray):
+    """U: (5, n) conserved -> (Q (5, n) primitives, c (n,), s (n,), floored (n,))."""
+    n = U.shape[1]
+    dU = _dev_f64(U)
+    dQ = torch.empty((5, n), dtype=torch.float64, device="cuda")
+    dc = torch.empty(n, dtype=torch.float64, device="cuda")
+    ds = torch.empty(n, dtype=torch.float64, device="cuda")
+    df = torch.empty(n, dtype=torch.int32, device="cuda")
+    abi.call(grid.lib, "orcha_unit_eos", grid.handle, n, ctypes.c_void_p(dU.data_ptr()),
+             ctypes.c_void_p(dQ.data_ptr()), ctypes.c_void_p(dc.data_ptr()), ctypes.c_void_p(ds.data_ptr()),
+             ctypes.c_void_p(df.data_ptr()), ctypes.c_void_p(_stream_ptr(None)))
+    torch.cuda.synchronize()
+    return dQ.cpu().numpy(), dc.cpu().numpy(), ds.cpu().numpy(), df.cpu().numpy()
+
+
+def orcha_unit_face_flux(grid: Grid, d: int, q: np.ndarray) -> np.ndarray:
+    """q: (4, 5, n) primitives of cells i-1 .. i+2 along d -> F (5, n) at i+1/2."""
+    n = q.shape[2]
+    dq = _dev_f64(q)
+    dF = torch.empty((5, n), dtype=torch.float64, device="cuda")
+    abi.call(grid.lib, "orcha_unit_face_flux", grid.handle, int(d), n, ctypes.c_void_p(dq.data_ptr()),
+             ctypes.c_void_p(dF.data_ptr()), ctypes.c_void_p(_stream_ptr(None)))
+    torch.cuda.synchronize()
+    return dF.cpu().numpy()
+
+
+def orcha_unit_riemann(grid: Grid, d: int, qL: np.ndarray, qR: np.ndarray) -> np.ndarray:
+    """qL, qR: (5, n) face-state primitives -> F (5, n)."""
+    n = qL.shape[1]
+    a, b = _dev_f64(qL), _dev_f64(qR)
+    dF = torch.empty((5, n), dtype=torch.float64, device="cuda")
+    abi.call(grid.lib, "orcha_unit_riemann", grid.handle, int(d), n, ctypes.c_void_p(a.data_ptr()),
+             ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(dF.data_ptr()), ctypes.c_void_p(_stream_ptr(None)))
+    torch.cuda.synchronize()
+    return dF.cpu().numpy()

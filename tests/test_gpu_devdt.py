@@ -77,15 +77,23 @@ def test_device_dt_through_nccl_single_rank():
         comm.destroy()
 
 
-def test_device_dt_refuses_local_communicator():
+def test_push_dt_refuses_nccl_communicator():
+    # orcha_comm_push_dt is the LOCAL transport's allgather; an NCCL
+    # communicator allgathers inside orcha_compute_dt(_device) instead
+    import ctypes
     from paper_2507_09337_b200 import abi, hydro
     g = H.make_grid(3, (8, 8, 8), (2, 1, 1))
-    owner = np.array([0, 1], dtype=np.int32)
-    comms = hydro.Comm.create_local(g, 2, owner)
-    pk = [hydro.Packet(g, [0])]
-    pk[0].pack(inp.to_blocks(inp.sedov(g.N), g.nb, [0]))
+    owner = np.zeros(g.nblocks, dtype=np.int32)
+    uid = (ctypes.c_uint8 * 128)()
+    abi.call(g.lib, "orcha_comm_unique_id", uid)
+    h = ctypes.c_void_p()
+    abi.call(g.lib, "orcha_comm_create", g.handle, uid, 1, 0, owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+             ctypes.byref(h))
+    comm = hydro.Comm(g, h, 1, 0, owner)
+    pk = H.gpu_setup(g, inp.sedov(g.N), 1)
     with pytest.raises(abi.OrchaError, match="ORCHA_E_ARG"):
-        hydro.orcha_compute_dt_device(pk, hydro.DevClock(), comms[0])
+        comm.push_dt(pk)
+    comm.destroy()
 
 
 def test_device_dt_reports_nonphysical_state():

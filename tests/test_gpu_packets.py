@@ -77,8 +77,9 @@ def test_many_packets_one_launch_fill_and_dt():
     assert np.array_equal(H.gather(g, pk), A)
 
 
+@pytest.mark.parametrize("parity", [False, True])
 @pytest.mark.parametrize("pipelined", [False, True])
-def test_streamed_host_mesh_equals_resident_run(pipelined):
+def test_streamed_host_mesh_equals_resident_run(pipelined, parity):
     # SURVEY 8(f) F3 / bench.py's e2e: the mesh lives in pinned host memory as
     # K packets shipped in (H2D streams), advanced, and shipped out with
     # orcha_packet_unpack_async (D2H streams) every step, the next step reading
@@ -86,11 +87,12 @@ def test_streamed_host_mesh_equals_resident_run(pipelined):
     # dt records right after its pack and its guard fill right after the next
     # slab's pack (orcha_packet_dt_records / orcha_fill_guardcells_packet;
     # z is not periodic, so a slab's guards read only its neighbour slabs),
-    # packets alternating over two copy streams each way
+    # packets alternating over two copy streams each way.  Parity build: also
+    # bitwise the oracle (state and every dt).
     import math
     import torch
     from paper_2507_09337_b200 import hydro
-    g = H.make_grid(3, (8, 8, 8), (4, 4, 4), bc=((R, O), (P, P), (O, R)))
+    g = H.make_grid(3, (8, 8, 8), (4, 4, 4), bc=((R, O), (P, P), (O, R)), parity=parity)
     U0 = inp.random_field(g.N, seed=51)
     A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
     slabs = [a for a in np.array_split(np.arange(g.nblocks), 4)]
@@ -144,6 +146,10 @@ def test_streamed_host_mesh_equals_resident_run(pipelined):
         out = inp.from_blocks(m.numpy(), g.N, g.nb, a, out)
     assert dts == [x[0] for x in logA]
     assert np.array_equal(out, A)
+    if parity:
+        Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4)
+        assert dts == olog.dts
+        assert np.array_equal(out, Oo)
 
 
 def test_per_packet_fill_arguments():

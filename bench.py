@@ -162,33 +162,73 @@ def run_reference(args, rank, world):
             "config": dict(workload_config(world), parallelism="cpu oracle, 1 thread (each step: a 64^3 sub-box "
                                                                            "sample of the same Sedov setup)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"64^3 3D Sedov, {args.steps} timed steps (plain C oracle, -O2 -ffp-contract=off)"},
+                             "sample": f"64^3 3D Sedov, {args.steps} timed steps (plain C oracle, -O2 -ffp-contract=off)",
+                             "host": host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(seconds_target=15.0):
-    """The oracle as it stands on this host (1 thread), on a bounded sample of
-    the workload: a 128^3 sub-box of the 3D Sedov setup, as many steps as fit
-    ~15 s (at least 1)."""
+def host_cpu():
+    """nproc and the CPU model of this host (recorded with the CPU baseline)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    if model is None and os.path.exists("/proc/cpuinfo"):
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def _oracle_rate(n, seconds_target, threads):
     import oracle
     import orcha_inputs as inp
 
+    used = oracle.use_threads(threads)
+    try:
+        og = oracle.Grid(N=(n, n, n))
+        U = oracle.padded(og, inp.sedov((n, n, n)))
+        steps = 0
+        t0 = time.perf_counter()
+        while True:
+            oracle.fill_ghosts(og, U)
+            r = oracle.compute_dt(og, U)
+            oracle.step(og, U, r.dt)
+            steps += 1
+            if time.perf_counter() - t0 > seconds_target:
+                break
+        el = time.perf_counter() - t0
+    finally:
+        oracle.use_threads(1)
+    return n ** 3 * steps / el, steps, el, used
+
+
+def cpu_baseline(seconds_target=12.0):
+    """The oracle as it stands on this host (1 thread), on a bounded sample of
+    the workload: a 96^3 sub-box of the 3D Sedov setup, as many steps as fit
+    ~12 s (at least 1); beside it the labelled oracle-omp variant (the same
+    source with -fopenmp over k-planes, bitwise the same results) on every
+    core of the host for ~8 s."""
     n = 96
-    og = oracle.Grid(N=(n, n, n))
-    U = oracle.padded(og, inp.sedov((n, n, n)))
-    steps = 0
-    t0 = time.perf_counter()
-    while True:
-        oracle.fill_ghosts(og, U)
-        r = oracle.compute_dt(og, U)
-        oracle.step(og, U, r.dt)
-        steps += 1
-        if time.perf_counter() - t0 > seconds_target:
-            break
-    el = time.perf_counter() - t0
-    return {"value": n ** 3 * steps / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n}^3 3D Sedov sub-box, {steps} steps (fill+dt+RK2), {el:.1f} s, 1 thread"}
+    v, steps, el, _ = _oracle_rate(n, seconds_target, 1)
+    cpu = host_cpu()
+    out = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"{n}^3 3D Sedov sub-box, {steps} steps (fill+dt+RK2), {el:.1f} s, 1 thread",
+           "host": cpu}
+    nthr = cpu["nproc"] or 1
+    if nthr > 1:
+        vo, so, elo, used = _oracle_rate(n, 8.0, nthr)
+        out["omp"] = {"value": vo, "unit": UNIT, "cores": used, "kind": "oracle-omp",
+                      "sample": f"{n}^3 3D Sedov sub-box, {so} steps, {elo:.1f} s, {used} OpenMP threads "
+                                "(bitwise the 1-thread result: tests/test_oracle_scheme.py)"}
+    return out
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -308,6 +348,59 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
     return out
 
 
+def other_workloads(stream):
+    """cell-updates/s of BASELINE.json's other configs (single GPU, device dt,
+    CUDA events around the timed steps after 3 warm-up steps): configs[0]
+    (2D Sedov, 4x4 blocks of 8^2), configs[1] (Sod: 1D 64 blocks x 16 cells
+    and the 2D tube of 64 x 1 blocks of 16^2), configs[2] (3D Sedov 128^3 as
+    512 blocks of 16^3), and a large 2D Sedov (2048^2 as 128 x 128 blocks of
+    16^2) so the 2D kernels are measured at a size that fills the GPU.  1D/2D
+    grids run the reference kernels (one thread per output cell; the fused
+    kernels cover 3D 8^3/16^3/32^3 blocks, DESIGN.md d2)."""
+    import numpy as np
+    import torch
+
+    import orcha_inputs as inp
+    from paper_2507_09337_b200 import hydro
+    P_, O_ = 1, 0
+    cases = {
+        "cfg1_sedov2d_32x32": dict(ndim=2, nb=(8, 8), nblk=(4, 4), ic=lambda N: inp.sedov(N), steps=200),
+        "cfg2_sod1d_1024": dict(ndim=1, nb=(16,), nblk=(64,), ic=lambda N: inp.sod(N), steps=200),
+        "cfg2_sod2d_tube_1024x16": dict(ndim=2, nb=(16, 16), nblk=(64, 1), bc=((O_, O_), (P_, P_), (O_, O_)),
+                                        xmax=(1.0, 16.0 / 1024), ic=lambda N: inp.sod(N), steps=200),
+        "cfg3_sedov3d_128": dict(ndim=3, nb=(16, 16, 16), nblk=(8, 8, 8), ic=lambda N: inp.sedov(N), steps=20),
+        "sedov2d_2048": dict(ndim=2, nb=(16, 16), nblk=(128, 128), ic=lambda N: inp.sedov(N), steps=20),
+    }
+    out = {}
+    for name, c in cases.items():
+        g = hydro.Grid(c["ndim"], c["nb"], c["nblk"], bc=c.get("bc", ((0, 0),) * 3),
+                       xmax=c.get("xmax", (1.0, 1.0, 1.0)))
+        nd = c["ndim"]
+        N = g.N[:nd]
+        pk = hydro.Packet(g, np.arange(g.nblocks))
+        pk.pack(inp.to_blocks(c["ic"](N), g.nb[:nd], pk.block_ids), stream)
+        clock = hydro.DevClock(0.0, math.inf)
+
+        def one():
+            hydro.orcha_fill_guardcells([pk], None, stream)
+            hydro.orcha_compute_dt_device([pk], clock, None, stream)
+            hydro.step_devdt([pk], clock.dt_tensor, None, stream)
+        for _ in range(3):
+            one()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(c["steps"]):
+            one()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / c["steps"]
+        cells = int(np.prod(N))
+        out[name] = {"value": cells / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "cells": cells,
+                     "steps": c["steps"], "kernels": "fused" if nd == 3 else "reference (one thread per cell)"}
+        del pk, g
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -322,6 +415,8 @@ def main():
     ap.add_argument("--e2e-packets", type=int, default=16,
                     help="streamed e2e: packets (z-slabs of the brick) shipped in and out every step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the phase-timing pass, the fp64 probe and the other-config throughputs")
     ap.add_argument("--variant", type=int, default=None, help="advance kernel variant (0 ref, 1 fused)")
     ap.add_argument("--method", default="telescoped", choices=["telescoped", "per-stage"],
                     help="RK2 step: the paper's telescoped step (default) or the per-stage F1 variant")
@@ -351,6 +446,9 @@ def main():
         raise SystemExit(f"--gpus must be one of {sorted(GPU_GRIDS)}")
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's own communicator lines (ranks, channels, NVLS / P2P transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0 and not os.path.exists(abi.library_path(False)):
         build.build()
@@ -492,6 +590,51 @@ def main():
                                           "finish; stage 1 + 2) captured in one CUDA graph, replayed"}
         del graph
 
+    # per-phase device times (a separate pass of the same steps with the
+    # library's phase events on; the timed loop above records none), per-rank
+    # busy fraction, measured fp64 peak, BASELINE's other configs
+    phases = None
+    fp64_probe = None
+    others = None
+    per_rank = None
+    if not args.no_extras:
+        hydro.orcha_set_phase_timing(lib, True)
+        hydro.orcha_phase_times(lib)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(args.steps):
+            step()
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pt = hydro.orcha_phase_times(lib)
+        hydro.orcha_set_phase_timing(lib, False)
+        pms = p0.elapsed_time(p1) / args.steps
+        phases = {k: v[0] / args.steps for k, v in pt.items()}
+        phases["step"] = pms
+        phases["note"] = ("ms per step: device time between each phase's CUDA events (library-recorded, "
+                          "orcha_set_phase_timing), separate pass of the same steps; fill includes the exchange, "
+                          "dt includes the allgather; gather fill mode on one GPU launches no fill kernel")
+        busy = (phases["fill"] + phases["dt"] + phases["stage1"] + phases["stage2"]) / pms
+        mine = torch.tensor([ms, adv_ms, busy, phases["exchange"], phases["dt_allgather"]], dtype=torch.float64,
+                            device="cuda")
+        if world > 1:
+            allr = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(allr, mine)
+        else:
+            allr = [mine]
+        per_rank = [{"rank": r, "ms_per_step": float(x[0]), "advance_ms": float(x[1]), "gpu_busy": float(x[2]),
+                     "exchange_ms": float(x[3]), "dt_allgather_ms": float(x[4])} for r, x in enumerate(allr)]
+        if rank == 0:
+            tinst, pms_probe = hydro.orcha_probe_fp64(lib, 20000, stream)
+            fp64_probe = {"tinst_per_s": tinst, "kernel_ms": pms_probe,
+                          "note": "measured DFMA thread-instructions/s / 1e12 (orcha_probe_fp64: 8 CTAs x 256 "
+                                  "threads per SM, 8 independent chains each)"}
+            if world == 1:
+                others = other_workloads(stream)
+
     # roofline of the dominant kernel (the advance): algorithmic bytes / flops
     pks = peaks()
     # (N > 1: the remote guards are exchanged into each rank's packet first;
@@ -510,6 +653,7 @@ def main():
                "unit": "T fp64-pipe inst/s", "frac": fp_achieved / pks["fp64_tinst"], "traffic": traffic,
                "traffic_source": traffic_src,
                "peak_source": "derived (DESIGN.md 6): 148 SM x 64 fp64 lanes x sm_max clock",
+               "peak_measured": fp64_probe["tinst_per_s"] if fp64_probe else None,
                "kernel": "hydro_advance (stage_fused_kernel<16,1> + <16,2>)",
                "algorithmic_fp64_instr_per_cell_update": fp_instr, "units_per_launch": cu_local}
     primary, other = (roof_fp, roof_hbm) if roof_fp["frac"] >= roof_hbm["frac"] else (roof_hbm, roof_fp)
@@ -561,6 +705,7 @@ def main():
             "advance_ms": adv_ms, "method": args.method, "dt_mode": args.dt_mode, "variants": variants,
             "clocks": clk, "gpu_launches": int(launches), "e2e": e2e, "e2e_serial": e2e_serial,
             "floor_hits": fh, "nonphysical_first_cell": bad,
+            "phases": phases, "per_rank": per_rank, "fp64_probe": fp64_probe, "other_configs": others,
         }
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()

@@ -356,6 +356,43 @@ int32_t orcha_set_guard_push(int32_t on);
 
 const char* orcha_last_error(void);
 
+/* Per-phase instrumentation (SURVEY 8(d) timing protocol).  Every
+ * phase the library enqueues -- ORCHA_PHASE_FILL (orcha_fill_guardcells*,
+ * including the exchange), ORCHA_PHASE_EXCHANGE (the cross-rank exchange
+ * alone), ORCHA_PHASE_DT (orcha_compute_dt*: record reduction, including the
+ * allgather), ORCHA_PHASE_DT_COMM (the dt allgather alone), ORCHA_PHASE_STAGE1
+ * and ORCHA_PHASE_STAGE2 (the two RK2 stage kernels of an advance, or of
+ * orcha_hydro_stage) -- is an NVTX range named "orcha:<phase>" on the host.
+ * With orcha_set_phase_timing(1) each phase also records a pair of CUDA
+ * events on its stream (off by default: no events in timed loops).
+ * orcha_phase_times synchronizes on every pair recorded since the previous
+ * query and writes the summed device milliseconds per phase to ms[0..5] and
+ * the number of occurrences to counts[0..5] (counts may be NULL); n >= 6.
+ * Call it between library calls, not concurrently with them.  Errors:
+ * ORCHA_E_ARG, ORCHA_E_CUDA. */
+enum { ORCHA_PHASE_FILL = 0, ORCHA_PHASE_EXCHANGE = 1, ORCHA_PHASE_DT = 2, ORCHA_PHASE_DT_COMM = 3,
+       ORCHA_PHASE_STAGE1 = 4, ORCHA_PHASE_STAGE2 = 5, ORCHA_NPHASES = 6 };
+int32_t orcha_set_phase_timing(int32_t on);
+int32_t orcha_phase_times(double* ms, int64_t* counts, int32_t n);
+
+/* FNV-1a 64-bit hash of `nbytes` host bytes, continuing from *hash (start
+ * from ORCHA_FNV1A64_OFFSET = 0xcbf29ce484222325; prime 0x100000001b3): the
+ * mesh checksum of SPEC S:L433 ("per-variable FNV-1a over raw bytes").  The
+ * binding's mesh_checksums / dump_mesh hash each variable over the blocks in
+ * ascending global id, cells in (k, j, i) order, little-endian fp64 -- the
+ * same value for any packet split or rank count.  Host only.
+ * Errors: ORCHA_E_ARG. */
+#define ORCHA_FNV1A64_OFFSET 0xcbf29ce484222325ULL
+int32_t orcha_fnv1a64(const void* data, size_t nbytes, uint64_t* hash);
+
+/* Measured fp64-pipe throughput of this GPU (the denominator of the bench's
+ * fp64 roofline beside the value derived from unit counts): one launch of 8
+ * SM-resident CTAs per SM, 8 independent DFMA chains of `iters` steps per
+ * thread, timed with CUDA events on `stream` (synchronizes).  Writes thread
+ * DFMA instructions per second / 1e12 and the kernel time.  Not part of the
+ * method.  Errors: ORCHA_E_ARG, ORCHA_E_CUDA. */
+int32_t orcha_probe_fp64(int32_t iters, double* tinst_per_s, double* ms, void* stream);
+
 /* ------------------------------------------------ unit entry points ----- */
 /* The per-cell / per-face device functions the fused kernels call, applied to
  * n independent inputs (test diagnostics for SURVEY 8(d)'s unit fuzz; the hot

@@ -35,6 +35,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "orcha_oracle.c")
 _LIB = os.path.join(_HERE, "liborcha_oracle.so")
+_LIB_OMP = os.path.join(_HERE, "liborcha_oracle_omp.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
 
 OUTFLOW, PERIODIC, REFLECT = 0, 1, 2
@@ -44,13 +45,25 @@ GAMMA_LAW, GAS_RADIATION = 0, 1   # EOS flag (SURVEY 8(f) F4 expensive-EOS surro
 TAG_CFL, TAG_CLAMP = 0, 1
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle shared library (gcc) if it is missing or stale."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".{os.getpid()}.tmp"
-        subprocess.run(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"], check=True)
-        os.replace(tmp, _LIB)
-    return _LIB
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile the oracle shared library (gcc) if it is missing or stale;
+    omp=True: the same source with -fopenmp ("oracle-omp", bitwise the same
+    results)."""
+    lib = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+        tmp = lib + f".{os.getpid()}.tmp"
+        subprocess.run(["gcc", *CFLAGS, *(["-fopenmp"] if omp else []), "-o", tmp, _SRC, "-lm"], check=True)
+        os.replace(tmp, lib)
+    return lib
+
+
+def use_threads(n: int) -> int:
+    """Switch this process's oracle to the -fopenmp build with n threads
+    (n <= 1: back to the plain build).  Returns the thread count in use."""
+    global _lib
+    _lib = None
+    _load(omp=n > 1)
+    return _lib.oracle_set_threads(int(n)) if n > 1 else 1
 
 
 class _CGrid(ctypes.Structure):
@@ -75,10 +88,12 @@ class _CGrid(ctypes.Structure):
 _lib = None
 
 
-def _load():
+def _load(omp: bool = False):
     global _lib
     if _lib is None:
-        lib = ctypes.CDLL(build())
+        lib = ctypes.CDLL(build(omp=omp))
+        lib.oracle_set_threads.argtypes = [ctypes.c_int]
+        lib.oracle_set_threads.restype = ctypes.c_int
         P = ctypes.POINTER
         d = ctypes.c_double
         dp = P(d)

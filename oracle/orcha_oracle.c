@@ -49,6 +49,20 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* "oracle-omp": the same source built with -fopenmp splits the
+ * k loops of the per-cell sweeps over threads.  Every cell's arithmetic and
+ * the order of its terms are unchanged (cells are independent; the floor-hit
+ * count is an integer sum), so the result is bitwise the single-threaded
+ * one.  Without -fopenmp the pragmas are absent. */
+#ifdef _OPENMP
+#include <omp.h>
+#define ORACLE_PAR_FOR _Pragma("omp parallel for schedule(static)")
+#define ORACLE_PAR_FOR_PRIMS _Pragma("omp parallel for schedule(static) reduction(+ : nh) reduction(| : bad)")
+#else
+#define ORACLE_PAR_FOR
+#define ORACLE_PAR_FOR_PRIMS
+#endif
+
 typedef struct {
   int32_t ndim;       /* 1, 2 or 3 */
   int32_t N[3];       /* interior cells per axis (1 on inactive axes) */
@@ -367,6 +381,8 @@ static double dxd(const oracle_grid* G, int d) { return (G->xmax[d] - G->xmin[d]
  * Returns -1 if a non-positive density was met. */
 static int prims_region(const oracle_grid* G, const double* U, double* Q, region R, int64_t* hits) {
   int bad = 0;
+  int64_t nh = 0;
+  ORACLE_PAR_FOR_PRIMS
   for (int64_t k = R.lo[2]; k < R.hi[2]; k++)
     for (int64_t j = R.lo[1]; j < R.hi[1]; j++)
       for (int64_t i = R.lo[0]; i < R.hi[0]; i++) {
@@ -374,9 +390,10 @@ static int prims_region(const oracle_grid* G, const double* U, double* Q, region
         for (int v = 0; v < 5; v++) u[v] = U[at(G, v, i, j, k)];
         int r = oracle_prim(G, u, q);
         if (r < 0) bad = 1;
-        if (r > 0) (*hits)++;
+        if (r > 0) nh++;
         for (int v = 0; v < 5; v++) Q[at(G, v, i, j, k)] = q[v];
       }
+  *hits += nh;
   return bad ? -1 : 0;
 }
 
@@ -390,6 +407,7 @@ static void divergence(const oracle_grid* G, const double* Q, region R, double* 
     double id = 1.0 / dxd(G, d);
     int64_t sh[3] = {0, 0, 0};
     sh[d] = 1;
+    ORACLE_PAR_FOR
     for (int64_t k = R.lo[2]; k < R.hi[2]; k++)
       for (int64_t j = R.lo[1]; j < R.hi[1]; j++)
         for (int64_t i = R.lo[0]; i < R.hi[0]; i++) {
@@ -494,6 +512,7 @@ int oracle_step(const oracle_grid* G, double* U, double dt, int32_t mode, double
   if (prims_region(G, U, Q, all, &hits)) bad = 1;
   divergence(G, Q, S1, D);
   for (int v = 0; v < 5; v++)
+    ORACLE_PAR_FOR
     for (int64_t k = S1.lo[2]; k < S1.hi[2]; k++)
       for (int64_t j = S1.lo[1]; j < S1.hi[1]; j++)
         for (int64_t i = S1.lo[0]; i < S1.hi[0]; i++) {
@@ -509,6 +528,7 @@ int oracle_step(const oracle_grid* G, double* U, double dt, int32_t mode, double
   if (prims_region(G, U1, Q, S1q, &hits)) bad = 1;
   divergence(G, Q, I, D);
   for (int v = 0; v < 5; v++)
+    ORACLE_PAR_FOR
     for (int64_t k = I.lo[2]; k < I.hi[2]; k++)
       for (int64_t j = I.lo[1]; j < I.hi[1]; j++)
         for (int64_t i = I.lo[0]; i < I.hi[0]; i++) {
@@ -521,4 +541,16 @@ int oracle_step(const oracle_grid* G, double* U, double dt, int32_t mode, double
   free(U1);
   if (floor_hits) *floor_hits += hits;
   return bad ? ORC_E_NONPHYSICAL : ORC_OK;
+}
+
+/* oracle-omp: thread count of the -fopenmp build (returns the count in use;
+ * 1 in the plain build). */
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
 }

@@ -20,6 +20,8 @@ RIEMANN_HLL, RIEMANN_HLLC = 0, 1
 LIMITER_MINMOD, LIMITER_MC = 0, 1
 EOS_GAMMA_LAW, EOS_GAS_RADIATION = 0, 1
 DT_CFL, DT_CLAMP = 0, 1
+FNV1A64_OFFSET = 0xcbf29ce484222325
+PHASES = ("fill", "exchange", "dt", "dt_allgather", "stage1", "stage2")
 
 EXPORTS = [
     "orcha_grid_create", "orcha_grid_destroy", "orcha_grid_nblocks", "orcha_packet_bytes", "orcha_packet_create",
@@ -32,7 +34,8 @@ EXPORTS = [
     "orcha_hydro_stage_devdt", "orcha_fill_guardcells_stage", "orcha_set_guard_push", "orcha_set_fill_mode",
     "orcha_packet_unpack_async", "orcha_fill_guardcells_packet", "orcha_packet_dt_records",
     "orcha_compute_dt_device", "orcha_unit_eos", "orcha_unit_face_flux", "orcha_unit_riemann",
-    "orcha_comm_push_dt",
+    "orcha_comm_push_dt", "orcha_set_phase_timing", "orcha_phase_times", "orcha_probe_fp64",
+    "orcha_fnv1a64",
 ]
 
 
@@ -132,6 +135,10 @@ _SIGS = {
     "orcha_hydro_stage_devdt": (_i32, [_vp, _i32, _vp, _vp]),
     "orcha_fill_guardcells_stage": (_i32, [_P(_vp), _i32, _vp, _i32, _vp]),
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),
+    "orcha_set_phase_timing": (_i32, [_i32]),
+    "orcha_phase_times": (_i32, [_P(_dbl), _P(_i64), _i32]),
+    "orcha_fnv1a64": (_i32, [_vp, _sz, _P(ctypes.c_uint64)]),
+    "orcha_probe_fp64": (_i32, [_i32, _P(_dbl), _P(_dbl), _vp]),
     "orcha_comm_push_dt": (_i32, [_vp, _P(_vp), _i32, _vp]),
     "orcha_unit_eos": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "orcha_unit_face_flux": (_i32, [_vp, _i32, _i64, _vp, _vp, _vp]),

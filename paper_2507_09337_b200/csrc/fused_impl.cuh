@@ -77,6 +77,16 @@
 #ifndef ORCHA_ROUNDS8
 #define ORCHA_ROUNDS8 0
 #endif
+// One CTA barrier per plane instead of two.  The faces of plane it+1 wait
+// only for the update warps to have read the face arrays of plane it (an
+// mbarrier) instead of a CTA barrier at the end of the plane.  ORCHA_ONEBAR=1:
+// the EOS of plane it+5 runs before the barrier that ends the faces phase;
+// =2: it stays after it (by the warps without update cells) and the z-face
+// tasks of plane it+1, the only readers of plane it+5 there, wait for it on a
+// second mbarrier.  0: two CTA barriers per plane.
+#ifndef ORCHA_ONEBAR
+#define ORCHA_ONEBAR 0
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 #ifndef ORCHA_ISSUE_LAST
 #define ORCHA_ISSUE_LAST 0
@@ -110,6 +120,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -242,8 +255,14 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
   __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
   if (GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
+  constexpr int UWARPS = (Gm::FZ + 31) / 32;  // warps with update cells
+  uint64_t* fdone = &bar[NS];  // ORCHA_ONEBAR: the update warps have read the face arrays of the plane
+  uint64_t* cdone = &bar[NS + 1];  // ORCHA_ONEBAR 2: the converting warps have converted plane it+5
+  constexpr bool CSPLIT = ORCHA_CONV_SPLIT && Gm::NW - UWARPS >= 2;
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
+    mbar_init(fdone, UWARPS);
+    mbar_init(cdone, CSPLIT ? Gm::NW - UWARPS : Gm::NW);
     fence_mbar_init();
   }
   __syncthreads();
@@ -407,6 +426,10 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     tbase[r] = kind < 3 ? task_base(kind, t) : 0;
   }
 
+  bool writes_faces = false;
+#pragma unroll
+  for (int r = 0; r < Gm::ROUNDS; r++) writes_faces |= tkind[r] < 3;
+
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
   const bool issuer = ORCHA_ISSUE_LAST ? warp == Gm::NW - 1 : warp == 0;  // the warp that stages planes
   if (issuer)
@@ -461,38 +484,59 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     }
     // phase 1: all face fluxes of the band's plane k (inputs: planes it+1 .. it+4)
     double* fz_cur = Fz + (it & 1) * 5 * Gm::FZ;
+    if (ORCHA_ONEBAR && it > 0 && writes_faces) mbar_wait(fdone, (it - 1) & 1);  // update(it-1) read the faces
 #pragma unroll
     for (int r = 0; r < Gm::ROUNDS; r++) {
       if (tkind[r] == 0) x_task(ttask[r], tbase[r], it);
       else if (tkind[r] == 1) y_task(ttask[r], tbase[r], it);
-      else if (tkind[r] == 2) z_task(ttask[r], tbase[r], it, fz_cur);
+      else if (tkind[r] == 2) {
+        if (ORCHA_ONEBAR == 2 && it > 0) mbar_wait(cdone, (it - 1) & 1);  // plane it+4 converted
+        z_task(ttask[r], tbase[r], it, fz_cur);
+      }
     }
+    constexpr int UW = UWARPS;
+    // the EOS of plane it+5 (read from iteration it+1 on; its copy was issued
+    // one plane earlier): ORCHA_ONEBAR before the barrier, else after it
+    auto convert_next = [&]() {
+      if (it + 5 < Gm::NPLANES) {
+        if constexpr (CSPLIT) {
+          if (warp >= UW) {
+            wait_plane(it + 5);
+            convert(it + 5, tid - UW * 32, NT - UW * 32);
+          }
+        } else {
+          wait_plane(it + 5);
+          convert(it + 5);
+        }
+      }
+      if (ORCHA_ONEBAR == 2 && (!CSPLIT || warp >= UW)) {  // plane it+5 is primitives
+        __syncwarp();
+        if (lane == 0) mbar_arrive(cdone);
+      }
+    };
+    if (ORCHA_ONEBAR == 1) convert_next();
     __syncthreads();
     // phase 2: stage plane it+6 into the slot of plane it+1 (read for the
     // last time in phase 1), convert plane it+5, update the band's cells
     if (issuer) issue(it + 6);
-    if (it + 5 < Gm::NPLANES) {
-      constexpr int UW = (Gm::FZ + 31) / 32;  // warps with update cells
-      if constexpr (ORCHA_CONV_SPLIT && Gm::NW - UW >= 2) {
-        if (warp >= UW) {
-          wait_plane(it + 5);
-          convert(it + 5, tid - UW * 32, NT - UW * 32);
-        }
-      } else {
-        wait_plane(it + 5);
-        convert(it + 5);
-      }
-    }
-    if (upd) {
+    if (ORCHA_ONEBAR != 1) convert_next();
+    if (upd || (ORCHA_ONEBAR && warp < UW)) {
       const double* fz_prev = Fz + ((it + 1) & 1) * 5 * Gm::FZ;
       double D[5];
+      if (upd) {
 #pragma unroll
-      for (int v = 0; v < 5; v++) {
-        double tx = (Fx[v * Gm::FX + lj * (W + 1) + li + 1] - Fx[v * Gm::FX + lj * (W + 1) + li]) * G.id[0];
-        double ty = (Fy[v * Gm::FY + (lj + 1) * W + li] - Fy[v * Gm::FY + lj * W + li]) * G.id[1];
-        double tz = (fz_cur[v * Gm::FZ + tid] - fz_prev[v * Gm::FZ + tid]) * G.id[2];
-        D[v] = (tx + ty) + tz;
+        for (int v = 0; v < 5; v++) {
+          double tx = (Fx[v * Gm::FX + lj * (W + 1) + li + 1] - Fx[v * Gm::FX + lj * (W + 1) + li]) * G.id[0];
+          double ty = (Fy[v * Gm::FY + (lj + 1) * W + li] - Fy[v * Gm::FY + lj * W + li]) * G.id[1];
+          double tz = (fz_cur[v * Gm::FZ + tid] - fz_prev[v * Gm::FZ + tid]) * G.id[2];
+          D[v] = (tx + ty) + tz;
+        }
       }
+      if (ORCHA_ONEBAR) {  // the face arrays of plane it are consumed: the faces of it+1 may overwrite them
+        __syncwarp();
+        if (lane == 0) mbar_arrive(fdone);
+      }
+      if (upd) {
       if (STAGE == 1) {
         double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
 #pragma unroll
@@ -523,8 +567,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         bool finite = isfinite(nw[0]) && isfinite(nw[1]) && isfinite(nw[2]) && isfinite(nw[3]) && isfinite(nw[4]);
         if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)g);
       }
+      }
     }
-    __syncthreads();
+    if (!ORCHA_ONEBAR) __syncthreads();
   }
   if (STAGE == 2) {
     block_reduce_rec<NT>(s_rec, g_rec);
@@ -606,16 +651,28 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
     static const int s2v = split_env("ORCHA_SPLIT2", 2);
     s2 = s2v;
-    if (s1 == 4) launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
-    else launch_stage<NB, 1, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    {
+      PhaseScope ph(PH_STAGE1, s);
+      if (s1 == 4) launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+      else launch_stage<NB, 1, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    }
+    PhaseScope ph(PH_STAGE2, s);
     if (s2 == 4) launch_stage<NB, 2, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
     else launch_stage<NB, 2, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
   } else if constexpr (NB == 32) {
-    launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    {
+      PhaseScope ph(PH_STAGE1, s);
+      launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    }
+    PhaseScope ph(PH_STAGE2, s);
     launch_stage<NB, 2, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
     s2 = 4;
   } else {
-    launch_stage<NB, 1, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    {
+      PhaseScope ph(PH_STAGE1, s);
+      launch_stage<NB, 1, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+    }
+    PhaseScope ph(PH_STAGE2, s);
     launch_stage<NB, 2, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
   }
   *nrecords = (long long)nslots * s2;
@@ -630,6 +687,7 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
                                    long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                    const NbrEntry* nbr, int pk) {
   constexpr int SP = (NB == 16) ? 2 : (NB == 32) ? 4 : 1;
+  PhaseScope ph(stage == 1 ? PH_STAGE1 : PH_STAGE2, s);
   if (stage == 1) {
     launch_stage<NB, 1, SP, 1, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nbr, pk);
   } else {

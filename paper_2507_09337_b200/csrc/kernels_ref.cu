@@ -119,10 +119,16 @@ static cudaError_t launch_ref(const DevGrid& G, double* state, double* u1, int n
   long long c1 = 1, c2 = 1;
   for (int d = 0; d < NDIM; d++) { c1 *= G.nb[d] + 4; c2 *= G.nb[d]; }
   long long t1 = nslots * c1, t2 = nslots * c2;
-  stage_ref_kernel<NDIM, 1><<<(unsigned)((t1 + 255) / 256), 256, 0, s>>>(G, state, u1, t1, slots, d_dt, h_dt,
-                                                                          records, st);
-  stage_ref_kernel<NDIM, 2><<<(unsigned)((t2 + 255) / 256), 256, 0, s>>>(G, state, u1, t2, slots, d_dt, h_dt,
-                                                                          records, st);
+  {
+    PhaseScope ph(PH_STAGE1, s);
+    stage_ref_kernel<NDIM, 1><<<(unsigned)((t1 + 255) / 256), 256, 0, s>>>(G, state, u1, t1, slots, d_dt, h_dt,
+                                                                            records, st);
+  }
+  {
+    PhaseScope ph(PH_STAGE2, s);
+    stage_ref_kernel<NDIM, 2><<<(unsigned)((t2 + 255) / 256), 256, 0, s>>>(G, state, u1, t2, slots, d_dt, h_dt,
+                                                                            records, st);
+  }
   count_launch(2);
   *nrecords = (t2 + 255) / 256;
   return cudaGetLastError();
@@ -146,6 +152,7 @@ static cudaError_t stage_ref(const DevGrid& G, int stage, double* state, double*
   for (int d = 0; d < NDIM; d++) c *= G.nb[d];
   long long t = nslots * c;
   unsigned blocks = (unsigned)((t + 255) / 256);
+  PhaseScope ph(stage == 1 ? PH_STAGE1 : PH_STAGE2, s);
   if (stage == 1) {
     stage_ref_kernel<NDIM, 1, 0><<<blocks, 256, 0, s>>>(G, state, u1, t, slots, d_dt, h_dt, records, st);
   } else {

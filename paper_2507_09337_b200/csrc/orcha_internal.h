@@ -187,4 +187,21 @@ cudaError_t launch_advance(const DevGrid& G, double* state, double* u1, int nslo
 // kernel variant selection (0 = reference per-cell kernels, 1 = fused z-marching)
 int kernel_variant();
 
+// Phases of the hot path (phases.cu): an NVTX range always, a CUDA-event pair
+// on the stream while orcha_set_phase_timing is on.  RAII: the scope's end
+// records the closing event.  Indices are ORCHA_PHASE_* of orcha.h.
+enum { PH_FILL = 0, PH_EXCHANGE = 1, PH_DT = 2, PH_DT_COMM = 3, PH_STAGE1 = 4, PH_STAGE2 = 5, PH_COUNT = 6 };
+class PhaseScope {
+ public:
+  PhaseScope(int phase, cudaStream_t s);
+  ~PhaseScope();
+  PhaseScope(const PhaseScope&) = delete;
+  PhaseScope& operator=(const PhaseScope&) = delete;
+
+ private:
+  int phase_;
+  cudaStream_t stream_;
+  int idx_;
+};
+
 }  // namespace orcha

@@ -720,8 +720,18 @@ static int32_t get_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fill
 
 // only >= 0: fill the guards of pk[only] alone (streamed packets: the set's
 // tables, every source resident, no exchange).
+static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer,
+                              bool faces_only, void* stream, int only);
+
+// The guard fill phase (incl. the exchange, which is also timed on its own).
 static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer, bool faces_only,
                          void* stream, int only = -1) {
+  PhaseScope ph(PH_FILL, (cudaStream_t)stream);
+  return fill_impl_body(pk, npk, comm, buffer, faces_only, stream, only);
+}
+
+static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer,
+                              bool faces_only, void* stream, int only) {
   if (!pk || npk < 1) return fail(ORCHA_E_ARG, "no packets");
   if (buffer != 0 && buffer != 1) return fail(ORCHA_E_ARG, "buffer must be 0 (state) or 1 (stage-1 state)");
   for (int q = 0; q < npk; q++) {
@@ -738,7 +748,10 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   if (f->has_remote) {
     CommPlan* cp = nullptr;  // cached by the communicator per packet set and buffer
     rc = comm_build_plan(comm, pk, npk, buffer, &cp);
-    if (rc == ORCHA_OK) rc = comm_exchange(comm, cp, s);
+    if (rc == ORCHA_OK) {
+      PhaseScope phx(PH_EXCHANGE, s);
+      rc = comm_exchange(comm, cp, s);
+    }
     if (rc) return rc;
   }
   // If every packet's last update of this buffer scattered itself into the
@@ -868,6 +881,7 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
   cudaStream_t s = (cudaStream_t)stream;
   std::vector<DtRecord> res(npk);
   std::vector<DevStatus> st(npk);
+  PhaseScope ph(PH_DT, s);
   {
     int32_t rc = ensure_dt_records(pk, npk, s);
     if (rc) return rc;
@@ -904,6 +918,7 @@ extern "C" int32_t orcha_compute_dt(orcha_packet* const* pk, int32_t npk, orcha_
     bad |= st[q].first_bad != ~0ull;
   }
   if (comm) {
+    PhaseScope phc(PH_DT_COMM, s);
     int32_t rc = comm_allreduce_dt(comm, &smax, &g, &bad, s);
     if (rc) return rc;
   }
@@ -959,11 +974,13 @@ extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk,
   if (!pk || npk < 1 || !d_clock) return fail(ORCHA_E_ARG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
   GatherRec* mine = nullptr;
+  PhaseScope ph(PH_DT, s);
   int32_t rc = rank_record(pk, npk, s, &mine);
   if (rc) return rc;
   const GatherRec* all = mine;
   int nall = 1;
   if (comm) {
+    PhaseScope phc(PH_DT_COMM, s);
     rc = comm_allgather_dt_device(comm, mine, &all, &nall, s);
     if (rc) return rc;
   }

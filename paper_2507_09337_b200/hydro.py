@@ -456,3 +456,91 @@ def orcha_unit_riemann(grid: Grid, d: int, qL: np.ndarray, qR: np.ndarray) -> np
              ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(dF.data_ptr()), ctypes.c_void_p(_stream_ptr(None)))
     torch.cuda.synchronize()
     return dF.cpu().numpy()
+
+
+# ---- instrumentation (include/orcha.h "per-phase instrumentation")
+def orcha_set_phase_timing(lib, on: bool):
+    abi.call(lib, "orcha_set_phase_timing", 1 if on else 0)
+
+
+def orcha_phase_times(lib) -> dict:
+    """{phase: (ms summed since the last query, occurrences)} (synchronizes)."""
+    ms = (ctypes.c_double * 6)()
+    cnt = (ctypes.c_int64 * 6)()
+    abi.call(lib, "orcha_phase_times", ms, cnt, 6)
+    return {name: (ms[i], cnt[i]) for i, name in enumerate(abi.PHASES)}
+
+
+def orcha_probe_fp64(lib, iters: int = 20000, stream=None):
+    """Measured fp64 DFMA thread-instructions/s / 1e12 and the probe kernel's ms."""
+    t, ms = ctypes.c_double(), ctypes.c_double()
+    abi.call(lib, "orcha_probe_fp64", int(iters), ctypes.byref(t), ctypes.byref(ms), ctypes.c_void_p(_stream_ptr(stream)))
+    return t.value, ms.value
+
+
+# ---- mesh checksums and dump (SPEC S:L433, S:L561; SURVEY 5)
+VAR_NAMES = ("rho", "rho_u", "rho_v", "rho_w", "E")
+
+
+def fnv1a64(lib, data: bytes, h: int = abi.FNV1A64_OFFSET) -> int:
+    hv = ctypes.c_uint64(h)
+    buf = ctypes.create_string_buffer(data, len(data))
+    abi.call(lib, "orcha_fnv1a64", ctypes.cast(buf, ctypes.c_void_p), len(data), ctypes.byref(hv))
+    return hv.value
+
+
+def _blocks_by_id(packets):
+    """{global block id: (5, nbz, nby, nbx) interior} over the packets (unpack, synchronizes)."""
+    out = {}
+    for p in packets:
+        arr = p.unpack()
+        for s, b in enumerate(p.block_ids):
+            out[int(b)] = arr[s]
+    return out
+
+
+def mesh_checksums(packets, blocks=None) -> dict:
+    """Per-variable FNV-1a 64 (hex) over the blocks in ascending global id,
+    cells in (k, j, i) order, little-endian fp64: independent of the packet split."""
+    lib = packets[0].lib
+    blocks = blocks if blocks is not None else _blocks_by_id(packets)
+    out = {}
+    for v, name in enumerate(VAR_NAMES):
+        h = abi.FNV1A64_OFFSET
+        for b in sorted(blocks):
+            h = fnv1a64(lib, np.ascontiguousarray(blocks[b][v], dtype="<f8").tobytes(), h)
+        out[name] = f"{h:016x}"
+    return out
+
+
+def dump_mesh(path: str, packets, t: Optional[float] = None, step: Optional[int] = None) -> dict:
+    """Raw mesh dump: `path`.bin = for each variable, for each block in
+    ascending global id, its interior cells (k, j, i order) as little-endian
+    fp64; `path`.json = the sidecar (dims, order, block ids, per-variable
+    checksums).  Returns the sidecar."""
+    import json
+    g = packets[0].grid
+    blocks = _blocks_by_id(packets)
+    ids = sorted(blocks)
+    with open(path + ".bin", "wb") as f:
+        for v in range(5):
+            for b in ids:
+                f.write(np.ascontiguousarray(blocks[b][v], dtype="<f8").tobytes())
+    side = {"format": "orcha-mesh-v1", "dtype": "<f8", "vars": list(VAR_NAMES),
+            "order": "var, block (ascending global id b = (bk*NBy + bj)*NBx + bi), k, j, i",
+            "ndim": g.ndim, "nb": list(g.nb), "nblk": list(g.nblk), "ng": g.ng, "N": list(g.N),
+            "xmin": list(g.desc.xmin), "xmax": list(g.desc.xmax), "block_ids": ids,
+            "checksums_fnv1a64": mesh_checksums(packets, blocks), "t": t, "step": step}
+    with open(path + ".json", "w") as f:
+        json.dump(side, f, indent=1)
+    return side
+
+
+def load_mesh(path: str):
+    """Inverse of dump_mesh: (sidecar, {block id: (5, nbz, nby, nbx)})."""
+    import json
+    side = json.load(open(path + ".json"))
+    nbz, nby, nbx = side["nb"][2], side["nb"][1], side["nb"][0]
+    ids = side["block_ids"]
+    raw = np.fromfile(path + ".bin", dtype="<f8").reshape(5, len(ids), nbz, nby, nbx)
+    return side, {b: np.ascontiguousarray(raw[:, s]) for s, b in enumerate(ids)}

@@ -153,3 +153,14 @@ def test_scheme_flags_validated(lib):
     rc, h = create(lib, d)
     assert rc == 0
     lib.orcha_grid_destroy(h)
+
+
+def test_fnv1a64_reference_vectors(lib):
+    # FNV-1a 64 test vectors (Fowler/Noll/Vo reference: "" -> offset basis,
+    # "a" -> 0xaf63dc4c8601ec8c, "foobar" -> 0x85944171f73967e8), host only
+    from paper_2507_09337_b200 import hydro
+    assert hydro.fnv1a64(lib, b"") == 0xcbf29ce484222325
+    assert hydro.fnv1a64(lib, b"a") == 0xaf63dc4c8601ec8c
+    assert hydro.fnv1a64(lib, b"foobar") == 0x85944171f73967e8
+    # continuation: hashing in pieces == hashing the concatenation
+    assert hydro.fnv1a64(lib, b"bar", hydro.fnv1a64(lib, b"foo")) == 0x85944171f73967e8

@@ -310,3 +310,22 @@ def test_reflect_wall_equals_mirrored_periodic_domain():
     Rr, logr = run_fresh(gr, base, nsteps=6)
     assert logd.dts == logr.dts
     assert np.array_equal(D[:, :, :, N:], Rr)
+
+
+def test_oracle_omp_build_is_bitwise_the_plain_build():
+    # SURVEY 8(d) "oracle-omp": the same source with -fopenmp over k-planes
+    # must give bitwise the single-threaded result (the bench's labelled
+    # multi-core CPU baseline relies on it)
+    N = (24, 20, 16)
+    g = oracle.Grid(N=N, bc=((P, P), (O, R), (O, O)))
+    U0 = inp.random_field(N, seed=17)
+    runs = []
+    for threads in (1, 4):
+        assert oracle.use_threads(threads) == threads
+        try:
+            runs.append(run_fresh(g, U0, nsteps=4))
+        finally:
+            oracle.use_threads(1)
+    (A, la), (B, lb) = runs
+    assert la.dts == lb.dts and la.floor_hits == lb.floor_hits
+    assert np.array_equal(A, B)

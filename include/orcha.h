@@ -454,6 +454,42 @@ int32_t orcha_comm_push(orcha_comm* comm, orcha_packet* const* packets, int32_t 
  * Errors: ORCHA_E_ARG (NCCL communicator, null argument), ORCHA_E_CUDA. */
 int32_t orcha_comm_push_dt(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, void* stream);
 
+/* F2 peer mode (the guard fill reads peer ranks' packets
+ * directly instead of exchanging, and dt is reduced by a one-shot peer write).
+ * Each rank registers its ONE packet (holding every block it owns).  Once all
+ * ranks have, orcha_fill_guardcells with this communicator builds neighbour
+ * and push tables that point into the other ranks' packets: the fill writes
+ * only x-guards (gather fill mode, fused kernels), stage 1 stages y/z guard
+ * rows straight from the owning block wherever it lives, stage 2 writes its
+ * new cells into the x-guards of the blocks they feed, on every rank -- no
+ * pack, send/recv or unpack.  Ordering across ranks is by a device-side
+ * barrier (system-scope counters; a wait beyond ~10 s sets an error flag read
+ * by orcha_comm_check instead of hanging): after a pack, before the first
+ * x-guard fill; between the two stage kernels of every advance (stage 2
+ * overwrites U^n in place while other ranks' stage 1 may read it); and in
+ * orcha_compute_dt(_device), which writes this rank's dt record into every
+ * rank's gather slot and then waits.  Each rank must therefore issue its
+ * calls on its OWN stream, concurrently with the others (a single stream
+ * serialising two ranks would wait forever at the first barrier -- and
+ * time out), and must not allocate device memory between the ranks'
+ * launches (CUDA's implicit synchronisation would serialise the streams):
+ * call orcha_fill_prepare for every rank first.  Available for LOCAL (virtual-rank) communicators, whose
+ * packets are directly addressable in one process (same-device "peers").
+ * Errors: ORCHA_E_ARG (NCCL communicator, packet of another grid, packet not
+ * holding exactly the rank's blocks), ORCHA_E_RANGE, ORCHA_E_CUDA. */
+int32_t orcha_comm_peer_register(orcha_comm* comm, orcha_packet* packet, void* stream);
+/* Build (and cache) the guard-fill plan of a packet set -- neighbour, push and
+ * exchange tables, uploaded with synchronous copies -- without filling.
+ * orcha_fill_guardcells builds it on first use anyway; call this first where
+ * a device allocation in the middle of a step would serialise streams (CUDA's
+ * implicit synchronisation): peer mode with virtual ranks on one device must
+ * prepare every rank after all have registered, before the first step.
+ * Errors: as orcha_fill_guardcells. */
+int32_t orcha_fill_prepare(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm);
+/* ORCHA_E_STATE if a peer barrier of this communicator timed out (device flag;
+ * synchronizes), else ORCHA_OK. */
+int32_t orcha_comm_check(orcha_comm* comm);
+
 /* Host-only view of the guard exchange plan between `rank` and `peer` (no
  * device work; for tests and tooling).  The plan is a pure function of the
  * grid and block_owner: the cells rank SENDS to peer are the sorted unique

@@ -35,7 +35,8 @@ EXPORTS = [
     "orcha_packet_unpack_async", "orcha_fill_guardcells_packet", "orcha_packet_dt_records",
     "orcha_compute_dt_device", "orcha_unit_eos", "orcha_unit_face_flux", "orcha_unit_riemann",
     "orcha_comm_push_dt", "orcha_set_phase_timing", "orcha_phase_times", "orcha_probe_fp64",
-    "orcha_fnv1a64",
+    "orcha_fnv1a64", "orcha_comm_peer_register", "orcha_comm_check",
+    "orcha_fill_prepare",
 ]
 
 
@@ -137,6 +138,9 @@ _SIGS = {
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),
     "orcha_set_phase_timing": (_i32, [_i32]),
     "orcha_phase_times": (_i32, [_P(_dbl), _P(_i64), _i32]),
+    "orcha_fill_prepare": (_i32, [_P(_vp), _i32, _vp]),
+    "orcha_comm_peer_register": (_i32, [_vp, _vp, _vp]),
+    "orcha_comm_check": (_i32, [_vp]),
     "orcha_fnv1a64": (_i32, [_vp, _sz, _P(ctypes.c_uint64)]),
     "orcha_probe_fp64": (_i32, [_i32, _P(_dbl), _P(_dbl), _vp]),
     "orcha_comm_push_dt": (_i32, [_vp, _P(_vp), _i32, _vp]),

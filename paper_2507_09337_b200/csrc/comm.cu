@@ -23,6 +23,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -248,6 +249,8 @@ struct CommPlan {
 // once destroyed; the hub goes when every slot is empty).
 struct Hub {
   std::vector<orcha_comm*> members;
+  std::vector<orcha_packet*> peer_packet;       // F2 peer mode: each virtual rank's registered packet
+  unsigned long long* d_ctr = nullptr;          // F2 peer mode: one barrier counter per virtual rank
   bool empty() const {
     for (auto* m : members)
       if (m) return false;
@@ -268,6 +271,11 @@ struct orcha_comm {
   std::vector<orcha::PeerBuf> bufs;      // same order as lists
   std::vector<orcha::CommPlan*> plans;
   void* d_gather = nullptr;              // allgather buffer: nranks * 32 B (+ 32 B send)
+  // F2 peer mode: peers' packets addressed directly
+  bool peer_mode = false;
+  unsigned long long** d_ctr_ptrs = nullptr;  // device array: every rank's barrier counter
+  unsigned long long bar_epoch = 0;           // barriers this rank has entered
+  int* d_err = nullptr;                       // device flag: a peer barrier timed out
 };
 
 namespace orcha {
@@ -381,6 +389,10 @@ static void free_plan(CommPlan* P) {
 void comm_drop_packet(orcha_packet* p) {
   std::lock_guard<std::mutex> lk(g_comm_mu);
   for (auto* c : g_comms)
+    if (c->hub)
+      for (auto*& q : c->hub->peer_packet)
+        if (q == p) q = nullptr;  // peer mode: the rank must register a packet again
+  for (auto* c : g_comms)
     for (size_t i = 0; i < c->plans.size();) {
       bool hit = false;
       for (auto* q : c->plans[i]->packets) hit |= q == p;
@@ -447,6 +459,16 @@ static int32_t gather_records(orcha_comm* c, const void* mine, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   if (mine != base) e = cudaMemcpyAsync(base, mine, 32, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "dt record copy");
+  if (c->peer_mode) {
+    // F2: one-shot P2P -- this rank's record into slot `rank` of every rank's
+    // gather buffer, then a device barrier: every slot is then filled
+    for (auto* m : c->hub->members) {
+      if (!m) return fail(ORCHA_E_STATE, "peer mode: a member rank was destroyed");
+      e = cudaMemcpyAsync((char*)m->d_gather + 32 + 32 * (size_t)c->rank, base, 32, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "dt record push (peer mode)");
+    }
+    return comm_peer_barrier(c, s);
+  }
   if (c->local) {
     e = cudaMemcpyAsync(base + 32 + 32 * (size_t)c->rank, base, 32, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "dt record copy (LOCAL)");
@@ -516,10 +538,68 @@ int32_t comm_push_dt_record(orcha_comm* c, const GatherRec* mine, cudaStream_t s
   return ORCHA_OK;
 }
 
+// ------------------------------------------------------ F2 peer mode ------
+// Device-side barrier over the ranks of a peer-mode communicator: every rank
+// adds 1 to every rank's counter (system-scope atomics: the counters live in
+// the ranks' own memory, reached by P2P), then waits until its own counter
+// reaches epoch * nranks.  Counters only grow, so no reset is needed.  A wait
+// longer than ~10 s (a rank that never arrives) sets the error flag and
+// returns instead of hanging the device.
+__global__ void peer_barrier_kernel(unsigned long long* const* ctr, int nranks, int me, unsigned long long target,
+                                    int* err, long long timeout_cycles) {
+  __threadfence_system();
+  for (int q = 0; q < nranks; q++) atomicAdd_system(ctr[q], 1ull);
+  const long long t0 = clock64();
+  while (true) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr[me]) : "memory");
+    if (v >= target) break;
+    if (clock64() - t0 > timeout_cycles) {
+      atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(200);
+  }
+  __threadfence_system();
+}
+
+int32_t comm_peer_barrier(orcha_comm* c, cudaStream_t s) {
+  if (!c->peer_mode || !c->d_ctr_ptrs) return fail(ORCHA_E_STATE, "peer barrier outside peer mode");
+  c->bar_epoch++;
+  // timeout: ~10 s at ~2 GHz; ORCHA_PEER_TIMEOUT_MS overrides (tests)
+  static const long long timeout = [] {
+    const char* e = getenv("ORCHA_PEER_TIMEOUT_MS");
+    return e ? (long long)atoll(e) * 2000000LL : 20000000000LL;
+  }();
+  peer_barrier_kernel<<<1, 1, 0, s>>>(c->d_ctr_ptrs, c->nranks, c->rank, c->bar_epoch * (unsigned long long)c->nranks,
+                                      c->d_err, timeout);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ORCHA_OK : cuda_fail(e, "peer barrier");
+}
+
+bool comm_peer_mode(const orcha_comm* c) { return c && c->peer_mode; }
+int comm_rank(const orcha_comm* c) { return c->rank; }
+
+// Every other rank's registered packet (peer mode); ORCHA_E_STATE until all
+// ranks have registered.
+int32_t comm_peer_packets(const orcha_comm* c, std::vector<orcha_packet*>* out) {
+  out->clear();
+  if (!c->peer_mode) return fail(ORCHA_E_STATE, "not in peer mode");
+  for (int q = 0; q < c->nranks; q++) {
+    orcha_packet* p = c->hub->peer_packet[q];
+    if (!p) return fail(ORCHA_E_STATE, "peer mode: rank " + std::to_string(q) + " has not registered its packet");
+    if (q != c->rank) out->push_back(p);
+  }
+  return ORCHA_OK;
+}
+
 static void destroy_comm(orcha_comm* c) {
   for (auto* p : c->plans) free_plan(p);
   for (auto& b : c->bufs) { cudaFree(b.d_send); cudaFree(b.d_recv); }
   cudaFree(c->d_gather);
+  cudaFree(c->d_ctr_ptrs);
+  cudaFree(c->d_err);
   if (c->nc && nccl().ok) nccl().CommDestroy(c->nc);
   delete c;
 }
@@ -613,6 +693,7 @@ extern "C" int32_t orcha_comm_push(orcha_comm* c, orcha_packet* const* pk, int32
 
 extern "C" int32_t orcha_comm_destroy(orcha_comm* c) {
   if (!c) return ORCHA_OK;
+  if (c->peer_mode) runtime_drop_comm(c);
   std::lock_guard<std::mutex> lk(g_comm_mu);
   g_comms.erase(std::remove(g_comms.begin(), g_comms.end(), c), g_comms.end());
   Hub* hub = c->hub;
@@ -620,7 +701,10 @@ extern "C" int32_t orcha_comm_destroy(orcha_comm* c) {
     // the slot stays (members are indexed by rank); pushes to it now fail
     for (auto*& m : hub->members)
       if (m == c) m = nullptr;
-    if (hub->empty()) delete hub;
+    if (hub->empty()) {
+      cudaFree(hub->d_ctr);
+      delete hub;
+    }
   }
   destroy_comm(c);
   return ORCHA_OK;
@@ -645,5 +729,53 @@ extern "C" int32_t orcha_comm_plan(const orcha_grid* g, int32_t nranks, int32_t 
   *count = (int64_t)v.size();
   if (out)
     for (long long i = 0; i < (long long)v.size() && i < cap; i++) out[i] = v[i];
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_comm_peer_register(orcha_comm* c, orcha_packet* p, void* stream) {
+  (void)stream;
+  if (!c || !p) return fail(ORCHA_E_ARG, "null argument");
+  if (!c->local)
+    return fail(ORCHA_E_ARG, "orcha_comm_peer_register: peer mode needs the ranks' packets addressable from this "
+                             "process (LOCAL virtual ranks); NCCL communicators use the exchange");
+  if (p->grid != c->grid) return fail(ORCHA_E_ARG, "packet of another grid");
+  for (long long b : p->ids)
+    if (c->owner[b] != c->rank) return fail(ORCHA_E_RANGE, "packet holds a block this rank does not own");
+  long long owned = 0;
+  for (long long b = 0; b < c->grid->nblocks; b++) owned += c->owner[b] == c->rank;
+  if ((long long)p->ids.size() != owned)
+    return fail(ORCHA_E_ARG, "peer mode needs ONE packet per rank holding every block the rank owns");
+  Hub* hub = c->hub;
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  if (hub->peer_packet.empty()) hub->peer_packet.assign(hub->members.size(), nullptr);
+  if (!hub->d_ctr) {
+    cudaError_t e = cudaMalloc(&hub->d_ctr, sizeof(unsigned long long) * hub->members.size());
+    if (e == cudaSuccess) e = cudaMemset(hub->d_ctr, 0, sizeof(unsigned long long) * hub->members.size());
+    if (e != cudaSuccess) return cuda_fail(e, "allocate peer barrier counters");
+  }
+  if (!c->d_ctr_ptrs) {
+    std::vector<unsigned long long*> ptrs(c->nranks);
+    for (int q = 0; q < c->nranks; q++) ptrs[q] = hub->d_ctr + q;
+    cudaError_t e = cudaMalloc(&c->d_ctr_ptrs, sizeof(void*) * c->nranks);
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_ctr_ptrs, ptrs.data(), sizeof(void*) * c->nranks, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int));
+    if (e != cudaSuccess) return cuda_fail(e, "peer barrier tables");
+  }
+  cudaFuncAttributes fa;  // load the barrier kernel now (lazy loading mid-step may wait for an idle device)
+  cudaError_t e = cudaFuncGetAttributes(&fa, peer_barrier_kernel);
+  if (e != cudaSuccess) return cuda_fail(e, "load peer barrier kernel");
+  hub->peer_packet[c->rank] = p;
+  c->peer_mode = true;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_comm_check(orcha_comm* c) {
+  if (!c) return fail(ORCHA_E_ARG, "null communicator");
+  if (!c->d_err) return ORCHA_OK;
+  int err = 0;
+  cudaError_t e = cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "read peer barrier flag");
+  if (err) return fail(ORCHA_E_STATE, "a peer barrier timed out (a rank never arrived)");
   return ORCHA_OK;
 }

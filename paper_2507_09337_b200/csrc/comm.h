@@ -21,4 +21,12 @@ int32_t comm_allgather_dt_device(orcha_comm* comm, const GatherRec* mine, const 
                                  cudaStream_t s);
 // LOCAL transport: push this virtual rank's record to every member.
 int32_t comm_push_dt_record(orcha_comm* comm, const GatherRec* mine, cudaStream_t s);
+// F2 peer mode: device barrier over the ranks (stage 1 -> stage 2, records
+// -> dt), the mode flag and the other ranks' registered packets.
+int32_t comm_peer_barrier(orcha_comm* comm, cudaStream_t s);
+bool comm_peer_mode(const orcha_comm* comm);
+int comm_rank(const orcha_comm* comm);
+int32_t comm_peer_packets(const orcha_comm* comm, std::vector<orcha_packet*>* out);
+// runtime.cu: drop the fill plans built on a peer-mode communicator being destroyed.
+void runtime_drop_comm(const orcha_comm* comm);
 }  // namespace orcha

@@ -576,6 +576,37 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     if (tid == 0) { rec[blockIdx.x].s = s_rec; rec[blockIdx.x].g = g_rec; }
   }
 }
+// The dynamic shared-memory attribute of every instantiation one launch_stage
+// may pick (once per process; also loads them under CUDA lazy loading).
+template <int NB, int STAGE, int SPLIT, int MODE, int SCH>
+static cudaError_t stage_attrs() {
+  using Gm = Geo<NB, STAGE, SPLIT, MODE>;
+  constexpr bool P2 = (STAGE == 2) || (MODE == 1);
+  constexpr bool GA = (STAGE == 1) || (MODE == 1);
+  static cudaError_t once = [] {
+    const int sm = (int)Gm::SMEM;
+    cudaError_t e = cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false, SCH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false, SCH>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if constexpr (GA)
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true, SCH>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if constexpr (P2)
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false, SCH>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if constexpr (P2 && GA)
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, true, SCH>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return e;
+  }();
+  return once;
+}
+
 template <int NB, int STAGE, int SPLIT, int MODE, int SCH>
 static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t s,
@@ -588,24 +619,7 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
   // telescoped stage 2 and both per-stage stages.
   constexpr bool P2 = (STAGE == 2) || (MODE == 1);
   constexpr bool GA = (STAGE == 1) || (MODE == 1);
-  static bool attr = false;
-  if (!attr) {
-    const int sm = (int)Gm::SMEM;
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false, SCH>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 1, false, SCH>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (GA)
-      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, true, SCH>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (P2)
-      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, false, SCH>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if constexpr (P2 && GA)
-      cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 2, true, SCH>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    attr = true;
-  }
+  stage_attrs<NB, STAGE, SPLIT, MODE, SCH>();
   // the guard-push epilogues and the gather staging are separate
   // instantiations so the default kernels carry none of their registers
   const dim3 grid(nslots * SPLIT);
@@ -642,40 +656,48 @@ static int split_env(const char* name, int dflt) {
   return (v == 2 || v == 4) ? v : dflt;
 }
 
+// parts: bit 0 = stage 1, bit 1 = stage 2 (F2 peer mode puts a cross-rank
+// barrier between the two launches).
 template <int NB, int SCH>
 static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
-                             cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk) {
+                             cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk, int parts) {
   int s2 = 1;
   if constexpr (NB == 16) {
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
     static const int s2v = split_env("ORCHA_SPLIT2", 2);
     s2 = s2v;
-    {
+    if (parts & 1) {
       PhaseScope ph(PH_STAGE1, s);
       if (s1 == 4) launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
       else launch_stage<NB, 1, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     }
-    PhaseScope ph(PH_STAGE2, s);
-    if (s2 == 4) launch_stage<NB, 2, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
-    else launch_stage<NB, 2, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    if (parts & 2) {
+      PhaseScope ph(PH_STAGE2, s);
+      if (s2 == 4) launch_stage<NB, 2, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+      else launch_stage<NB, 2, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    }
   } else if constexpr (NB == 32) {
-    {
+    if (parts & 1) {
       PhaseScope ph(PH_STAGE1, s);
       launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     }
-    PhaseScope ph(PH_STAGE2, s);
-    launch_stage<NB, 2, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    if (parts & 2) {
+      PhaseScope ph(PH_STAGE2, s);
+      launch_stage<NB, 2, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    }
     s2 = 4;
   } else {
-    {
+    if (parts & 1) {
       PhaseScope ph(PH_STAGE1, s);
       launch_stage<NB, 1, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
     }
-    PhaseScope ph(PH_STAGE2, s);
-    launch_stage<NB, 2, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    if (parts & 2) {
+      PhaseScope ph(PH_STAGE2, s);
+      launch_stage<NB, 2, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nullptr, pk);
+    }
   }
-  *nrecords = (long long)nslots * s2;
+  if (parts & 2) *nrecords = (long long)nslots * s2;
   return cudaGetLastError();
 }
 
@@ -697,13 +719,27 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
   return cudaGetLastError();
 }
 
+// Load (CUDA lazy loading) the telescoped gather-mode kernels of this block
+// size and scheme ahead of time, with their shared-memory attribute: loading
+// mid-step may wait for an idle device (F2 peer mode: a rank spinning in a
+// barrier never lets it go idle).
+template <int NB, int SCH>
+static cudaError_t preload_nb() {
+  constexpr int S1 = NB == 16 ? 2 : NB == 32 ? 4 : 1;
+  cudaError_t e = stage_attrs<NB, 1, S1, 0, SCH>();
+  if (e == cudaSuccess) e = stage_attrs<NB, 2, S1, 0, SCH>();
+  return e;
+}
+
 // The exported entry points of one (block size, scheme) translation unit.
 #define ORCHA_FUSED_TU(NB, SCH)                                                                                  \
   cudaError_t fused_advance_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,             \
                                            const SlotInfo* slots, const double* d_dt, double h_dt,              \
                                            DtRecord* records, long long* nrecords, DevStatus* st,               \
-                                           cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk) { \
-    return launch_nb<NB, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk); \
+                                           cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk,   \
+                                           int parts) {                                                         \
+    return launch_nb<NB, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk, \
+                              parts);                                                                            \
   }                                                                                                              \
   cudaError_t fused_stage_n##NB##_s##SCH(const DevGrid& G, int stage, double* state, double* u1, int nslots,    \
                                          const SlotInfo* slots, const double* d_dt, double h_dt,                \
@@ -711,6 +747,7 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
                                          cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk) {  \
     return launch_stage_nb<NB, SCH>(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s,   \
                                     push, nbr, pk);                                                              \
-  }
+  }                                                                                                              \
+  cudaError_t fused_preload_n##NB##_s##SCH() { return preload_nb<NB, SCH>(); }
 
 }  // namespace orcha

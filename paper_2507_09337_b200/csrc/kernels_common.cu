@@ -351,4 +351,19 @@ cudaError_t launch_dt_reduce_multi(const PacketDt* pd, int npk, DtRecord* out, D
   return cudaGetLastError();
 }
 
+// Load (CUDA lazy loading) every kernel of this unit the device-dt step and
+// the fill use, ahead of time: loading a module mid-step can wait for the
+// device to go idle, which a rank spinning in a peer barrier never does.
+cudaError_t common_preload() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, fill_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, fill_x_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_kernel<3>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_reduce_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_gather_rec_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_finish_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, status_reset_kernel);
+  return e;
+}
+
 }  // namespace orcha

@@ -8,11 +8,13 @@ namespace orcha {
   cudaError_t fused_advance_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,             \
                                            const SlotInfo* slots, const double* d_dt, double h_dt,              \
                                            DtRecord* records, long long* nrecords, DevStatus* st,               \
-                                           cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk); \
+                                           cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk,   \
+                                           int parts);                                                          \
   cudaError_t fused_stage_n##NB##_s##SCH(const DevGrid& G, int stage, double* state, double* u1, int nslots,    \
                                          const SlotInfo* slots, const double* d_dt, double h_dt,                \
                                          DtRecord* records, long long* nrecords, DevStatus* st,                 \
-                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk);
+                                         cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk); \
+  cudaError_t fused_preload_n##NB##_s##SCH();
 ORCHA_FUSED_DECL(8, 0)
 ORCHA_FUSED_DECL(8, 1)
 ORCHA_FUSED_DECL(16, 0)
@@ -44,7 +46,7 @@ bool fused_supported(const DevGrid& G) {
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
                                  DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr,
-                                 bool push_x_only) {
+                                 bool push_x_only, int parts) {
   const int pk = push_x_only ? 2 : 1;
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
@@ -52,7 +54,7 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
   // so the paper-path kernels keep their register allocation
   const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
 #define ORCHA_ADV(NB, SCH) \
-  fused_advance_n##NB##_s##SCH(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk)
+  fused_advance_n##NB##_s##SCH(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s, push, nbr, pk, parts)
   if (G.nb[0] == 16) return var ? ORCHA_ADV(16, 1) : ORCHA_ADV(16, 0);
   if (G.nb[0] == 32) return var ? ORCHA_ADV(32, 1) : ORCHA_ADV(32, 0);
   return var ? ORCHA_ADV(8, 1) : ORCHA_ADV(8, 0);
@@ -79,6 +81,17 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
   if (G.nb[0] == 32) return var ? ORCHA_STG(32, 1) : ORCHA_STG(32, 0);
   return var ? ORCHA_STG(8, 1) : ORCHA_STG(8, 0);
 #undef ORCHA_STG
+}
+
+// Load the kernels a step of this grid will launch (see preload_nb).
+cudaError_t common_preload();
+cudaError_t fused_preload(const DevGrid& G) {
+  cudaError_t e = common_preload();
+  if (e != cudaSuccess || !fused_supported(G)) return e;
+  const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
+  if (G.nb[0] == 16) return var ? fused_preload_n16_s1() : fused_preload_n16_s0();
+  if (G.nb[0] == 32) return var ? fused_preload_n32_s1() : fused_preload_n32_s0();
+  return var ? fused_preload_n8_s1() : fused_preload_n8_s0();
 }
 
 }  // namespace orcha

@@ -146,6 +146,10 @@ struct orcha_packet {
   bool u1_xpushed;
   bool u1_guards_xonly;
   const orcha::NbrEntry* d_nbr_u1;
+  // F2 peer mode: the communicator whose ranks' packets this one's last fill
+  // addressed directly (the advance then puts a cross-rank barrier between
+  // its stage kernels); nullptr otherwise
+  orcha_comm* peer_comm = nullptr;
 };
 
 namespace orcha {

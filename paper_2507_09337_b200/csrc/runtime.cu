@@ -57,7 +57,7 @@ cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int 
 cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                  const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
                                  DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr,
-                                 bool push_x_only);
+                                 bool push_x_only, int parts = 3);
 cudaError_t launch_stage_ref(const DevGrid& G, int stage, double* state, double* u1, int nslots,
                              const SlotInfo* slots, const double* d_dt, double h_dt, DtRecord* records,
                              long long* nrecords, DevStatus* st, cudaStream_t s);
@@ -66,6 +66,7 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
                                long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                const NbrEntry* nbr, bool push_x_only);
 bool fused_supported(const DevGrid& G);
+cudaError_t fused_preload(const DevGrid& G);
 }  // namespace orcha
 
 // Fill mode: 1 = gather (default): when every guard source of the packet set
@@ -213,6 +214,8 @@ struct FillPlan {
   std::vector<NbrEntry*> d_cross_u1;
   CommPlan* remote = nullptr;        // guard cells sourced from other ranks (comm.cu)
   bool has_remote = false;
+  orcha_comm* peer = nullptr;        // F2 peer mode: other ranks' blocks addressed directly (no exchange)
+  std::vector<orcha_packet*> sources;  // every packet the tables point into (own + peer mode's other ranks')
   // gather mode with remote sources: some y/z-guard row of the packet has a
   // remote source while one of its x-guard parts has a resident one
   std::vector<char> edge_fix;
@@ -263,12 +266,33 @@ static std::vector<DtPlan*> g_dtplans;
 static std::mutex g_plan_mu;
 static std::vector<FillPlan*> g_plans;
 
+namespace orcha {
+// A peer-mode communicator is going away: forget the plans built on it (their
+// tables point into its ranks' packets) and detach its packets.
+void runtime_drop_comm(const orcha_comm* c) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (size_t i = 0; i < g_plans.size();) {
+    FillPlan* f = g_plans[i];
+    if (f->peer == c) {
+      for (auto* q : f->packets) {
+        if (q->push_plan == f) { q->push_plan = nullptr; q->d_push = q->d_push_u1 = nullptr; }
+        if (q->peer_comm == c) { q->peer_comm = nullptr; q->guards_valid = false; }
+      }
+      free_plan_tables(f);
+      g_plans.erase(g_plans.begin() + i);
+    } else {
+      i++;
+    }
+  }
+}
+}  // namespace orcha
+
 static void drop_plans_with(orcha_packet* p) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
   for (size_t i = 0; i < g_plans.size();) {
     FillPlan* f = g_plans[i];
     bool hit = false;
-    for (auto* q : f->packets) hit |= (q == p);
+    for (auto* q : f->sources) hit |= (q == p);
     if (hit) {
       for (auto* q : f->packets)
         if (q->push_plan == f) { q->push_plan = nullptr; q->d_push = q->d_push_u1 = nullptr; }
@@ -512,11 +536,25 @@ static HostEntry make_entry(const orcha_grid* g, const int bc[3], const int o[3]
   return h;
 }
 
-static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, FillPlan** out) {
-  const orcha_grid* g = pk[0]->grid;
+static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm, FillPlan** out) {
+  const orcha_grid* g = pk_in[0]->grid;
   const DevGrid& G = g->dev;
+  // F2 peer mode: the other ranks' packets join the set as sources and push
+  // targets (their pointers, reached directly; cross-rank barriers order the
+  // accesses), so nothing is exchanged.  ext = this rank's packets, then theirs.
+  const bool peer = comm_peer_mode(comm);
+  std::vector<orcha_packet*> ext(pk_in, pk_in + npk);
+  if (peer) {
+    if (npk != 1) return fail(ORCHA_E_ARG, "peer mode: one packet per rank");
+    std::vector<orcha_packet*> others;
+    int32_t rc = comm_peer_packets(comm, &others);
+    if (rc) return rc;
+    ext.insert(ext.end(), others.begin(), others.end());
+  }
+  orcha_packet* const* pk = ext.data();
+  const int next = (int)ext.size();
   std::unordered_map<long long, std::pair<int, int>> where;  // block -> (packet, slot)
-  for (int q = 0; q < npk; q++) {
+  for (int q = 0; q < next; q++) {
     if (pk[q]->grid != g) return fail(ORCHA_E_ARG, "packets belong to different grids");
     for (int s = 0; s < pk[q]->nslots; s++)
       if (!where.emplace(pk[q]->ids[s], std::make_pair(q, s)).second)
@@ -524,6 +562,8 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
   }
   FillPlan* f = new FillPlan();
   f->packets.assign(pk, pk + npk);
+  f->peer = peer ? comm : nullptr;
+  f->sources = ext;
   for (int q = 0; q < npk; q++) {
     orcha_packet* p = pk[q];
     std::vector<NbrEntry> tab((size_t)p->nslots * 27);
@@ -562,7 +602,7 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     std::vector<NbrEntry> tab1 = tab;
     for (auto& e : tab1)
       if (e.src) {
-        for (int q2 = 0; q2 < npk; q2++) {
+        for (int q2 = 0; q2 < next; q2++) {
           orcha_packet* sp = pk[q2];
           if (e.src >= sp->state && e.src < sp->state + (long long)sp->nslots * kNVar * G.cube) {
             e.src = sp->scratch + (e.src - sp->state);
@@ -608,9 +648,11 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
         e.mode = h.mode;
         e.flip = h.flip;
         // same packet only: a push into another packet's guards would land
-        // before that packet's own advance has read them (stage 1)
+        // before that packet's own advance has read them (stage 1) -- except
+        // into other ranks' packets in peer mode, whose stage 1 ends before
+        // any stage 2 starts (the cross-rank barrier between the stages)
         auto it = where.find(h.src_block);
-        e.dst = (it == where.end() || it->second.first != q)
+        e.dst = (it == where.end() || (it->second.first != q && !(peer && it->second.first >= npk)))
                     ? nullptr
                     : pk[it->second.first]->state + (long long)it->second.second * kNVar * G.cube;
       }
@@ -618,7 +660,7 @@ static int32_t build_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fi
     pt1 = pt;
     for (auto& e : pt1)
       if (e.dst)
-        for (int q2 = 0; q2 < npk; q2++) {
+        for (int q2 = 0; q2 < next; q2++) {
           orcha_packet* sp = pk[q2];
           if (e.dst >= sp->state && e.dst < sp->state + (long long)sp->nslots * kNVar * G.cube) {
             e.dst = sp->scratch + (e.dst - sp->state);
@@ -708,7 +750,8 @@ static int32_t get_plan(orcha_packet* const* pk, int npk, orcha_comm* comm, Fill
     if ((int)f->packets.size() != npk) continue;
     bool same = true;
     for (int q = 0; q < npk; q++) same &= f->packets[q] == pk[q];
-    if (same && (!f->has_remote || comm)) { *out = f; return ORCHA_OK; }
+    const orcha_comm* want_peer = comm_peer_mode(comm) ? comm : nullptr;
+    if (same && f->peer == want_peer && (!f->has_remote || comm)) { *out = f; return ORCHA_OK; }
   }
   FillPlan* f = nullptr;
   int32_t rc = build_plan(pk, npk, comm, &f);
@@ -769,6 +812,20 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
   const DevGrid& G0 = pk[0]->grid->dev;
   const bool xonly = buffer == 0 && npk == 1 && !push_enabled() && fill_mode() == 1 &&
                      kernel_variant() == 1 && fused_supported(G0);
+  if (f->peer) {
+    // F2 peer mode: the gather fill only (x-guards; stage 1 stages y/z rows
+    // from the owners, other ranks' included, and stage 2 pushes x-guards
+    // into them); the telescoped method only
+    if (!xonly || only >= 0)
+      return fail(ORCHA_E_STATE, "peer mode needs the gather fill (fill mode 1, fused kernels, one packet, no "
+                                 "guard push) and the telescoped method");
+    if (!(pk[0]->xguards_pushed && pk[0]->push_plan == f)) {
+      // after a pack: the x-guard fill reads other ranks' interiors, so every
+      // rank's pack must be done (device barrier)
+      rc = comm_peer_barrier(f->peer, s);
+      if (rc) return rc;
+    }
+  }
   // per-stage stage-1 buffer in gather mode: stage 1 wrote the U1 x-guards
   // (same plan), stage 2 stages the y/z rows of U1 from their owners
   const bool xonly_u1 = buffer == 1 && npk == 1 && !push_enabled() && fill_mode() == 1 && kernel_variant() == 1 &&
@@ -806,6 +863,10 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
       // the last advance scattered U^{n+1} into the x-guards with this plan: nothing to do
       if (pk[q]->xguards_pushed && pk[q]->push_plan == f) continue;
       e = launch_fill_x(G0, dst, pk[q]->nslots, f->d_tables[q], s);
+      if (e == cudaSuccess && f->peer) {  // every rank's x-guards before any rank's stage 1 reads them
+        rc = comm_peer_barrier(f->peer, s);
+        if (rc) return rc;
+      }
     } else {
       const NbrEntry* tab = all_pushed ? (buffer ? f->d_cross_u1[q] : f->d_cross[q])   // cross-packet only
                                        : (buffer ? f->d_tables_u1[q] : f->d_tables[q]);
@@ -819,6 +880,7 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
     pk[q]->d_push = f->d_push[q];
     pk[q]->d_push_u1 = f->d_push_u1[q];
     pk[q]->push_plan = f;
+    pk[q]->peer_comm = buffer ? pk[q]->peer_comm : f->peer;
     if (buffer) {
       pk[q]->u1_guards_valid = true;
       pk[q]->u1_guards_xonly = false;
@@ -832,6 +894,24 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
     }
   }
   return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_fill_prepare(orcha_packet* const* pk, int32_t npk, orcha_comm* comm) {
+  if (!pk || npk < 1) return fail(ORCHA_E_ARG, "no packets");
+  for (int q = 0; q < npk; q++)
+    if (!pk[q]) return fail(ORCHA_E_ARG, "null packet");
+  FillPlan* f = nullptr;
+  int32_t rc = get_plan(pk, npk, comm, &f);
+  if (rc) return rc;
+  if (f->has_remote) {
+    CommPlan* cp = nullptr;
+    rc = comm_build_plan(comm, pk, npk, 0, &cp);
+    if (rc) return rc;
+  }
+  // and load the step's kernels now (CUDA lazy loading would otherwise load
+  // them at their first launch, which may wait for an idle device)
+  cudaError_t e = fused_preload(pk[0]->grid->dev);
+  return e == cudaSuccess ? ORCHA_OK : cuda_fail(e, "preload kernels");
 }
 
 extern "C" int32_t orcha_fill_guardcells(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, void* stream) {
@@ -1018,9 +1098,23 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   if (!fused)
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
-  else
+  else if (!p->peer_comm)
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                              &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr, xpush);
+  else {
+    // F2 peer mode: stage 2 overwrites U^n in place and pushes x-guards into
+    // other ranks' blocks, whose stage 1 reads them: every rank's stage 1
+    // ends before any stage 2 starts
+    if (!p->guards_xonly || !xpush) return fail(ORCHA_E_STATE, "peer mode: gather-mode fill expected");
+    e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
+                             p->status, s, push, p->d_nbr, xpush, 1);
+    if (e == cudaSuccess) {
+      int32_t rc = comm_peer_barrier(p->peer_comm, s);
+      if (rc) return rc;
+      e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
+                               &p->nrecords, p->status, s, push, p->d_nbr, xpush, 2);
+    }
+  }
   if (e != cudaSuccess) return cuda_fail(e, "advance kernels");
   if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
   p->guards_valid = false;

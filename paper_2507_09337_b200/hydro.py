@@ -194,6 +194,14 @@ class Comm:
         arr, n = _handles(packets)
         abi.call(self.lib, "orcha_comm_push", self.handle, arr, n, int(buffer), ctypes.c_void_p(_stream_ptr(stream)))
 
+    def peer_register(self, packet, stream=None):
+        """F2 peer mode: this rank's one packet becomes addressable by the other ranks."""
+        abi.call(self.lib, "orcha_comm_peer_register", self.handle, packet.handle,
+                 ctypes.c_void_p(_stream_ptr(stream)))
+
+    def check(self):
+        abi.call(self.lib, "orcha_comm_check", self.handle)
+
     def push_dt(self, packets, stream=None):
         """LOCAL transport: publish this virtual rank's dt record to every member."""
         arr, n = _handles(packets)
@@ -227,6 +235,11 @@ def orcha_fill_guardcells(packets, comm=None, stream=None):
     lib = packets[0].lib
     abi.call(lib, "orcha_fill_guardcells", arr, n, comm.handle if comm is not None else None,
              ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def orcha_fill_prepare(packets, comm=None):
+    arr, n = _handles(packets)
+    abi.call(packets[0].lib, "orcha_fill_prepare", arr, n, comm.handle if comm is not None else None)
 
 
 def orcha_fill_guardcells_packet(packets, index: int, stream=None):

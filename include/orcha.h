@@ -454,6 +454,22 @@ int32_t orcha_comm_push(orcha_comm* comm, orcha_packet* const* packets, int32_t 
  * Errors: ORCHA_E_ARG (NCCL communicator, null argument), ORCHA_E_CUDA. */
 int32_t orcha_comm_push_dt(orcha_comm* comm, orcha_packet* const* packets, int32_t npackets, void* stream);
 
+/* Interior/boundary overlap (SURVEY 8(e) "Overlap"; the paper's streams
+ * hiding transfers): one telescoped step of this rank's single
+ * packet -- orcha_compute_dt_device into d_clock, then the guard exchange on
+ * a library-owned stream while stage 1 runs on the packet's LEADING interior
+ * slots (blocks whose 26 neighbours are all in this packet, so they read
+ * nothing the exchange writes); stage 1 of the remaining slots waits for the
+ * exchange, stage 2 runs on all.  Order the packet's block_ids interior-first
+ * to get any overlap.  Results are bitwise those of orcha_fill_guardcells ->
+ * orcha_compute_dt_device -> orcha_hydro_advance_devdt, which is also what
+ * runs when there is nothing to overlap (first step after a pack, no remote
+ * source, an owner map whose gather fill needs the complement pass, no
+ * leading interior slot).  Gather fill mode and the fused kernels; a LOCAL
+ * communicator needs every rank's orcha_comm_push (and orcha_comm_push_dt)
+ * first, as for orcha_fill_guardcells.  Errors: as those calls. */
+int32_t orcha_hydro_step_overlap(orcha_packet* packet, orcha_comm* comm, orcha_dev_clock* d_clock, void* stream);
+
 /* F2 peer mode (the guard fill reads peer ranks' packets
  * directly instead of exchanging, and dt is reduced by a one-shot peer write).
  * Each rank registers its ONE packet (holding every block it owns).  Once all

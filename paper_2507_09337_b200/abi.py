@@ -36,7 +36,7 @@ EXPORTS = [
     "orcha_compute_dt_device", "orcha_unit_eos", "orcha_unit_face_flux", "orcha_unit_riemann",
     "orcha_comm_push_dt", "orcha_set_phase_timing", "orcha_phase_times", "orcha_probe_fp64",
     "orcha_fnv1a64", "orcha_comm_peer_register", "orcha_comm_check",
-    "orcha_fill_prepare",
+    "orcha_fill_prepare", "orcha_hydro_step_overlap",
 ]
 
 
@@ -138,6 +138,7 @@ _SIGS = {
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),
     "orcha_set_phase_timing": (_i32, [_i32]),
     "orcha_phase_times": (_i32, [_P(_dbl), _P(_i64), _i32]),
+    "orcha_hydro_step_overlap": (_i32, [_vp, _vp, _vp, _vp]),
     "orcha_fill_prepare": (_i32, [_P(_vp), _i32, _vp]),
     "orcha_comm_peer_register": (_i32, [_vp, _vp, _vp]),
     "orcha_comm_check": (_i32, [_vp]),

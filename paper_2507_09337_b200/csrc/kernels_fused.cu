@@ -94,4 +94,8 @@ cudaError_t fused_preload(const DevGrid& G) {
   return var ? fused_preload_n8_s1() : fused_preload_n8_s0();
 }
 
+// Doubles per (slot, var) cube of the telescoped U1 scratch ((n+4)^3, origin
+// -2, 256-byte aligned; u1_cube<NB> in fused_impl.cuh).
+long long fused_u1_cube(int nb) { return ((long long)(nb + 4) * (nb + 4) * (nb + 4) * 8 + 255) / 256 * 256 / 8; }
+
 }  // namespace orcha

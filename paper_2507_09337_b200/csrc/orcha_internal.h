@@ -150,6 +150,10 @@ struct orcha_packet {
   // addressed directly (the advance then puts a cross-rank barrier between
   // its stage kernels); nullptr otherwise
   orcha_comm* peer_comm = nullptr;
+  // interior/boundary overlap (orcha_hydro_step_overlap): a library-owned
+  // side stream for the exchange and two events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
 };
 
 namespace orcha {

@@ -67,6 +67,7 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
                                const NbrEntry* nbr, bool push_x_only);
 bool fused_supported(const DevGrid& G);
 cudaError_t fused_preload(const DevGrid& G);
+long long fused_u1_cube(int nb);
 }  // namespace orcha
 
 // Fill mode: 1 = gather (default): when every guard source of the packet set
@@ -404,6 +405,9 @@ extern "C" int32_t orcha_packet_destroy(orcha_packet* p) {
   drop_plans_with(p);
   comm_drop_packet(p);
   cudaFree(p->d_slots);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->ev_ready) cudaEventDestroy(p->ev_ready);
+  if (p->ev_halo) cudaEventDestroy(p->ev_halo);
   delete p;
   return ORCHA_OK;
 }
@@ -1134,6 +1138,121 @@ extern "C" int32_t orcha_hydro_advance(orcha_packet* p, double dt, void* stream)
 extern "C" int32_t orcha_hydro_advance_devdt(orcha_packet* p, const double* d_dt, void* stream) {
   if (!d_dt) return fail(ORCHA_E_ARG, "null d_dt");
   return advance_impl(p, d_dt, 0.0, stream);
+}
+
+// ------------------------------------ interior/boundary overlap (8(e)) ---
+// One telescoped step of a rank's single packet with the halo exchange in
+// flight while stage 1 runs on the packet's leading interior slots (blocks
+// whose 26 neighbours are all resident: they read nothing the exchange
+// writes); stage 1 of the remaining slots waits for the exchange, then stage 2
+// runs on every slot.  dt is computed first (device clock), as in
+// orcha_compute_dt_device.  Falls back to fill -> dt -> advance when there is
+// nothing to overlap (no remote source, first step after a pack, a non-brick
+// owner map needing the complement pass, no leading interior slot).
+static int interior_prefix(const orcha_packet* p, const FillPlan* f) {
+  // the table of slot s is f->d_tables[0] + 27 s on the device; recompute on
+  // the host from the ids: a slot is interior when every neighbour block is
+  // resident in this packet (or the slot itself across a physical boundary)
+  const orcha_grid* g = p->grid;
+  const DevGrid& G = g->dev;
+  std::unordered_map<long long, int> mine;
+  for (int s = 0; s < p->nslots; s++) mine[p->ids[s]] = s;
+  (void)f;
+  int n = 0;
+  for (; n < p->nslots; n++) {
+    long long b = p->ids[n];
+    int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
+                 (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+    bool ok = true;
+    for (int dd = 0; dd < 27 && ok; dd++) {
+      int o[3] = {dd % 3 - 1, (dd / 3) % 3 - 1, dd / 9 - 1};
+      bool valid = true;
+      for (int a = g->desc.ndim; a < 3; a++) valid &= (o[a] == 0);
+      if (!valid) continue;
+      ok = mine.count(make_entry(g, bc, o).src_block) > 0;
+    }
+    if (!ok) break;
+  }
+  return n;
+}
+
+extern "C" int32_t orcha_hydro_step_overlap(orcha_packet* p, orcha_comm* comm, orcha_dev_clock* d_clock,
+                                            void* stream) {
+  if (!p || !comm || !d_clock) return fail(ORCHA_E_ARG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  orcha_packet* pk[1] = {p};
+  FillPlan* f = nullptr;
+  int32_t rc = get_plan(pk, 1, comm, &f);
+  if (rc) return rc;
+  const DevGrid& G = p->grid->dev;
+  const bool gather = !push_enabled() && fill_mode() == 1 && kernel_variant() == 1 && fused_supported(G);
+  const bool steady = p->xguards_pushed && p->push_plan == f;
+  const int nint = (f->has_remote && gather && steady && !f->edge_fix[0] && !f->peer) ? interior_prefix(p, f) : 0;
+  if (nint == 0) {  // nothing to overlap: the plain sequence
+    rc = fill_impl(pk, 1, comm, 0, false, stream);
+    if (rc == ORCHA_OK) rc = orcha_compute_dt_device(pk, 1, comm, d_clock, stream);
+    if (rc == ORCHA_OK) rc = advance_impl(p, &d_clock->dt, 0.0, stream);
+    return rc;
+  }
+  if (!p->side) {
+    cudaError_t e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_halo, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "overlap stream");
+  }
+  CommPlan* cp = nullptr;
+  rc = comm_build_plan(comm, pk, 1, 0, &cp);
+  if (rc) return rc;
+  // dt first (its allgather precedes the exchange on the communicator)
+  rc = orcha_compute_dt_device(pk, 1, comm, d_clock, stream);
+  if (rc) return rc;
+  cudaError_t e = cudaEventRecord(p->ev_ready, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->side, p->ev_ready, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "overlap fork");
+  {
+    PhaseScope phf(PH_FILL, p->side);
+    PhaseScope phx(PH_EXCHANGE, p->side);
+    rc = comm_exchange(comm, cp, p->side);
+  }
+  if (rc) return rc;
+  e = cudaEventRecord(p->ev_halo, p->side);
+  if (e != cudaSuccess) return cuda_fail(e, "overlap join");
+  // the fill's bookkeeping (what fill_impl records for a gather-mode fill)
+  p->d_push = f->d_push[0];
+  p->d_push_u1 = f->d_push_u1[0];
+  p->push_plan = f;
+  p->guards_valid = true;
+  p->guards_xonly = true;
+  p->d_nbr = f->d_tables[0];
+  p->guards_full = true;
+  const double* d_dt = &d_clock->dt;
+  const long long c5 = (long long)kNVar * G.cube, u5 = (long long)kNVar * fused_u1_cube(G.nb[0]);
+  // stage 1 on the interior slots [0, nint) while the halo is in flight
+  e = launch_advance_fused(G, p->state, p->scratch, nint, p->d_slots, d_dt, 0.0, p->records, &p->nrecords,
+                           p->status, s, p->d_push, p->d_nbr, true, 1);
+  if (e == cudaSuccess && nint < p->nslots) {
+    e = cudaStreamWaitEvent(s, p->ev_halo, 0);
+    if (e == cudaSuccess)
+      e = launch_advance_fused(G, p->state + nint * c5, p->scratch + nint * u5, p->nslots - nint, p->d_slots + nint,
+                               d_dt, 0.0, p->records, &p->nrecords, p->status, s, p->d_push, p->d_nbr + 27LL * nint,
+                               true, 1);
+  } else if (e == cudaSuccess) {
+    e = cudaStreamWaitEvent(s, p->ev_halo, 0);
+  }
+  if (e == cudaSuccess)
+    e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, 0.0, p->records, &p->nrecords,
+                             p->status, s, p->d_push, p->d_nbr, true, 2);
+  if (e != cudaSuccess) return cuda_fail(e, "advance kernels (overlap)");
+  if (p->nrecords > p->records_cap) return fail(ORCHA_E_LAYOUT, "record capacity exceeded (internal)");
+  p->guards_valid = false;
+  p->guards_pushed = false;
+  p->xguards_pushed = true;
+  p->records_valid = true;
+  p->stage1_done = false;
+  p->u1_guards_valid = false;
+  p->u1_pushed = false;
+  p->u1_xpushed = p->u1_guards_xonly = false;
+  return ORCHA_OK;
 }
 
 // ------------------------------------------- per-stage variant (F1) ------

@@ -237,6 +237,42 @@ def orcha_fill_guardcells(packets, comm=None, stream=None):
              ctypes.c_void_p(_stream_ptr(stream)))
 
 
+def orcha_hydro_step_overlap(packet: Packet, comm, clock: DevClock, stream=None):
+    """One step with the halo exchange overlapping stage 1 of the interior slots."""
+    abi.call(packet.lib, "orcha_hydro_step_overlap", packet.handle, comm.handle, ctypes.c_void_p(clock.ptr),
+             ctypes.c_void_p(_stream_ptr(stream)))
+
+
+def interior_first(nblk: Sequence[int], bc, owner, rank: int, ndim: int = 3) -> np.ndarray:
+    """The block ids `rank` owns, ordered interior-first: blocks whose 26
+    neighbours (periodic wrap; a clamp / mirror side counts as the block
+    itself) are all owned by `rank` come first (ascending id), then the
+    rest.  Host bookkeeping for orcha_hydro_step_overlap."""
+    nblk = list(nblk) + [1] * (3 - len(nblk))
+    owner = np.asarray(owner)
+    ids = np.flatnonzero(owner == rank)
+    inner, outer = [], []
+    for b in ids:
+        c0 = [b % nblk[0], (b // nblk[0]) % nblk[1], b // (nblk[0] * nblk[1])]
+        ok = True
+        for oz in (-1, 0, 1):
+            for oy in (-1, 0, 1):
+                for ox in (-1, 0, 1):
+                    o = (ox, oy, oz)
+                    if any(o[a] != 0 for a in range(ndim, 3)):
+                        continue
+                    c = []
+                    for a in range(3):
+                        x = c0[a] + o[a]
+                        if x < 0 or x >= nblk[a]:
+                            x = x % nblk[a] if bc[a][0 if x < 0 else 1] == abi.BC_PERIODIC else c0[a]
+                        c.append(x)
+                    nbk = (c[2] * nblk[1] + c[1]) * nblk[0] + c[0]
+                    ok &= bool(owner[nbk] == rank)
+        (inner if ok else outer).append(int(b))
+    return np.array(inner + outer, dtype=np.int64)
+
+
 def orcha_fill_prepare(packets, comm=None):
     arr, n = _handles(packets)
     abi.call(packets[0].lib, "orcha_fill_prepare", arr, n, comm.handle if comm is not None else None)

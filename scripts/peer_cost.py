@@ -6,6 +6,9 @@ rank, gather fill mode, device-resident dt.
 * exchange: the NCCL path's plan, pack, copy and unpack kernels (LOCAL
   transport: a device copy stands in for ncclSend/Recv) and the dt records
   pushed to every rank, all ranks on one stream;
+* overlap: the same exchange with stage 1 of each rank's interior blocks
+  (interior-first slot order) running while its halo is unpacked on a side
+  stream (orcha_hydro_step_overlap);
 * peer (F2): every rank on its own stream, stage 1 staging other ranks' rows
   directly, stage 2 pushing x-guards into them, device barriers between the
   stage kernels and before the dt reduction -- no pack / copy / unpack.
@@ -29,7 +32,7 @@ import orcha_inputs as inp  # noqa: E402
 from paper_2507_09337_b200 import abi, hydro  # noqa: E402
 
 
-def setup(grid):
+def setup(grid, interior_first=False):
     px, py, pz = grid
     R = px * py * pz
     BB, NB = bench.BRICK_BLOCKS, bench.NB
@@ -40,7 +43,7 @@ def setup(grid):
     comms = hydro.Comm.create_local(g, R, owner)
     pks = []
     for r in range(R):
-        ids = np.flatnonzero(owner == r)
+        ids = hydro.interior_first(nblk, ((0, 0),) * 3, owner, r) if interior_first else np.flatnonzero(owner == r)
         p = hydro.Packet(g, ids)
         p.pack(inp.sedov_packet(N, NB, ids, xmax=(float(px), float(py), float(pz))))
         pks.append(p)
@@ -86,6 +89,21 @@ def measure(grid, steps=10, warmup=3):
             hydro.orcha_compute_dt_device([pks[r]], clocks[r], comms[r], s)
             hydro.orcha_hydro_advance_devdt(pks[r], clocks[r].dt_tensor, s)
     out["exchange_ms_per_rank_step"] = timed(step_x, [s], steps, warmup) / R
+    for c in comms:
+        c.destroy()
+    del pks
+    # exchange path with the interior/boundary overlap (orcha_hydro_step_overlap)
+    g, comms, pks = setup(grid, interior_first=True)
+    clocks = [hydro.DevClock() for _ in range(R)]
+
+    def step_o():
+        for r in range(R):
+            comms[r].push([pks[r]], s)
+        for r in range(R):
+            comms[r].push_dt([pks[r]], s)
+        for r in range(R):
+            hydro.orcha_hydro_step_overlap(pks[r], comms[r], clocks[r], s)
+    out["overlap_ms_per_rank_step"] = timed(step_o, [s], steps, warmup) / R
     for c in comms:
         c.destroy()
     del pks
@@ -136,6 +154,7 @@ def main():
     for r in rows:
         r["exchange_overhead_vs_single"] = r["exchange_ms_per_rank_step"] / one - 1.0
         r["peer_overhead_vs_single"] = r["peer_ms_per_rank_step"] / one - 1.0
+        r["overlap_overhead_vs_single"] = r["overlap_ms_per_rank_step"] / one - 1.0
     print(json.dumps({"single_rank_ms_per_step": one, "rows": rows, "gpu": torch.cuda.get_device_name(0),
                       "note": "virtual ranks on one GPU, each with cfg4's 4096-block brick; per-rank step = "
                               "the R-rank step / R; no NVLink wire time is included in either path"}))

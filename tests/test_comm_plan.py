@@ -162,3 +162,22 @@ def test_gloo_two_rank_halo_exchange():
         p.join(timeout=60)
     assert sorted(r for r, _, _ in res) == [0, 1]
     assert all(ok for _, ok, _ in res), res
+
+
+def test_interior_first_ordering():
+    # hydro.interior_first: a rank's blocks whose 26 neighbours it owns come
+    # first; for cfg4's (2,2,2) bricks of 16^3 blocks with outflow walls that
+    # is the 15^3 blocks away from the three internal faces
+    from paper_2507_09337_b200 import hydro
+    nblk, brick, gg = (32, 32, 32), (16, 16, 16), (2, 2, 2)
+    owner = hydro.brick_owner(nblk, brick, gg)
+    bc = ((0, 0),) * 3
+    ids = hydro.interior_first(nblk, bc, owner, 0)
+    assert sorted(ids.tolist()) == np.flatnonzero(owner == 0).tolist()
+    inner = 15 ** 3
+    bi, bj, bk = ids % 32, (ids // 32) % 32, ids // 1024
+    assert np.all((bi[:inner] < 15) & (bj[:inner] < 15) & (bk[:inner] < 15))
+    assert not np.any((bi[inner:] < 15) & (bj[inner:] < 15) & (bk[inner:] < 15))
+    # periodic x: the wrap neighbour belongs to the other x-brick, so the x = 0 face is boundary too
+    ids_p = hydro.interior_first(nblk, ((1, 1), (0, 0), (0, 0)), owner, 0)
+    assert np.all((ids_p[:14 * 15 * 15] % 32 >= 1))

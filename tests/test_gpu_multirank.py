@@ -213,3 +213,73 @@ def test_nccl_single_rank_communicator():
     assert [x[0] for x in log] == [x[0] for x in logB]
     assert np.array_equal(A, B)
     comm.destroy()
+
+
+def _run_overlap(g, U0, owner, nsteps):
+    """Virtual ranks stepping with orcha_hydro_step_overlap (interior-first slots)."""
+    from paper_2507_09337_b200 import hydro
+    nd = g.ndim
+    n = int(owner.max()) + 1
+    comms = hydro.Comm.create_local(g, n, owner)
+    pks = []
+    for r in range(n):
+        ids = hydro.interior_first(g.nblk, [tuple(g.desc.bc[a]) for a in range(3)], owner, r, nd)
+        p = hydro.Packet(g, ids)
+        p.pack(inp.to_blocks(U0, g.nb[:nd], p.block_ids))
+        pks.append(p)
+    clocks = [hydro.DevClock() for _ in range(n)]
+    log = []
+    for _ in range(nsteps):
+        for r in range(n):
+            comms[r].push([pks[r]])
+        for r in range(n):
+            comms[r].push_dt([pks[r]])
+        for r in range(n):
+            hydro.orcha_hydro_step_overlap(pks[r], comms[r], clocks[r])
+        recs = [(c.dt, c.smax, c.argmax, c.tag) for c in (k.read() for k in clocks)]
+        assert all(x == recs[0] for x in recs), recs
+        log.append(recs[0])
+    out = H.gather(g, pks)
+    for c in comms:
+        c.destroy()
+    return out, log
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_overlap_step_bitwise_equal_single_domain(case):
+    # SURVEY 8(e) "Overlap": stage 1 of the interior blocks runs while the
+    # halo is in flight; bitwise the sequential step
+    from paper_2507_09337_b200 import hydro
+    ndim, nb, nblk, bc, gg, brick = case
+    g = H.make_grid(ndim, nb, nblk, bc=bc)
+    owner = hydro.brick_owner(nblk, brick, gg)
+    U0 = inp.sedov(g.N[:ndim]) if bc[0][0] == O else inp.random_field(g.N[:ndim], seed=33)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=5)
+    B, logB = _run_overlap(g, U0, owner, 5)
+    assert logB == [tuple(x) for x in logA]
+    assert np.array_equal(A, B)
+
+
+def test_overlap_step_parity_build_equals_oracle():
+    from paper_2507_09337_b200 import hydro
+    ndim, nb, nblk, bc, gg, brick = CASES[1]
+    g = H.make_grid(ndim, nb, nblk, bc=bc, parity=True)
+    owner = hydro.brick_owner(nblk, brick, gg)
+    U0 = inp.random_field(g.N, seed=34)
+    B, logB = _run_overlap(g, U0, owner, 4)
+    Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4)
+    assert [x[0] for x in logB] == olog.dts
+    assert np.array_equal(B, Oo)
+
+
+def test_overlap_step_scattered_owners_falls_back_bitwise():
+    # a non-brick owner map needs the gather fill's complement pass: the call
+    # runs the plain sequence, with the same results
+    g = H.make_grid(3, (8, 8, 8), (4, 3, 2), bc=((R, O), (P, P), (O, R)))
+    owner = (np.random.default_rng(4).random(g.nblocks) * 3).astype(np.int32)
+    owner[:3] = [0, 1, 2]
+    U0 = inp.random_field(g.N, seed=35)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=3)
+    B, logB = _run_overlap(g, U0, owner, 3)
+    assert [x[0] for x in logB] == [x[0] for x in logA]
+    assert np.array_equal(A, B)

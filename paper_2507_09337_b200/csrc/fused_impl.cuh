@@ -87,6 +87,14 @@
 #ifndef ORCHA_ONEBAR
 #define ORCHA_ONEBAR 0
 #endif
+// z-face carry (ORCHA_ZCARRY, per stage: bit 0 stage 1, bit 1 stage 2): the
+// z-face task of a column computes the z-slope of cell k+1 once and keeps
+// its upper face state q + s/2 (the left state of face k+3/2) in a
+// per-column shared slot for the next plane, instead of recomputing that
+// slope there (one slope per z-face instead of two; bitwise the same values)
+#ifndef ORCHA_ZCARRY
+#define ORCHA_ZCARRY 1
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 #ifndef ORCHA_ISSUE_LAST
 #define ORCHA_ISSUE_LAST 0
@@ -168,8 +176,10 @@ struct Geo {
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
+  static constexpr bool ZC = (ORCHA_ZCARRY >> (STAGE - 1)) & 1;  // z-face carry slots
   static constexpr size_t SMEM =
-      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ) + 64 + ((NS * IR + 15) / 16) * 16;
+      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ + (ZC ? 5 * FZ : 0)) + 64 +
+      ((NS * IR + 15) / 16) * 16;
   // CTAs per SM we aim for: shared memory bound (227 KB per SM), at most 4
   static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
   static constexpr int MINB_R = 65536 / (NT * 80);  // at ~80 registers per thread
@@ -238,7 +248,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   double* Fx = ring + NS * 5 * BAND;                     // [5][H][W+1]
   double* Fy = Fx + 5 * Gm::FX;                          // [5][H+1][W]
   double* Fz = Fy + 5 * Gm::FY;                          // [2][5][H][W]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Fz + 2 * 5 * Gm::FZ);
+  double* Zc = Fz + 2 * 5 * Gm::FZ;                      // [5][H][W] z-face carry (Gm::ZC)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Zc + (Gm::ZC ? 5 * Gm::FZ : 0));
   unsigned char* flipm = reinterpret_cast<unsigned char*>(bar + 8);  // [NS][IR]
 
   const int tid = threadIdx.x;
@@ -403,12 +414,41 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   };
   // z-face k+1/2 of column (i, j): stencil planes it+1 .. it+4 (z = k-1 .. k+2)
   auto z_task = [&](int w, int base, int it, double* fz_out) {
-    Prim q0, q1, q2, q3;
-    ld(ring + ((it + 1) % NS) * 5 * BAND, base, q0);
-    ld(ring + ((it + 2) % NS) * 5 * BAND, base, q1);
-    ld(ring + ((it + 3) % NS) * 5 * BAND, base, q2);
-    ld(ring + ((it + 4) % NS) * 5 * BAND, base, q3);
-    face_flux<2, SCH>(q0, q1, q2, q3, G, fz_out + w, Gm::FZ);
+    if constexpr (Gm::ZC) {
+      // left state of cell k: carried from the previous plane (the prologue
+      // face seeds it); cells k, k+1, k+2 give cell k+1's two face states
+      Prim L, R, Up, q0, q1, q2;
+      if (it >= 0) {
+        L.r = Zc[w];
+        L.u = Zc[Gm::FZ + w];
+        L.v = Zc[2 * Gm::FZ + w];
+        L.w = Zc[3 * Gm::FZ + w];
+        L.p = Zc[4 * Gm::FZ + w];
+      } else {
+        Prim qm;
+        ld(ring + ((it + 1) % NS) * 5 * BAND, base, qm);
+        ld(ring + ((it + 2) % NS) * 5 * BAND, base, q0);
+        ld(ring + ((it + 3) % NS) * 5 * BAND, base, q1);
+        plm_cell<SCH>(qm, q0, q1, G, &L, &R);
+      }
+      ld(ring + ((it + 2) % NS) * 5 * BAND, base, q0);
+      ld(ring + ((it + 3) % NS) * 5 * BAND, base, q1);
+      ld(ring + ((it + 4) % NS) * 5 * BAND, base, q2);
+      plm_cell<SCH>(q0, q1, q2, G, &Up, &R);
+      Zc[w] = Up.r;
+      Zc[Gm::FZ + w] = Up.u;
+      Zc[2 * Gm::FZ + w] = Up.v;
+      Zc[3 * Gm::FZ + w] = Up.w;
+      Zc[4 * Gm::FZ + w] = Up.p;
+      riemann_store<2, SCH>(L, R, G, fz_out + w, Gm::FZ);
+    } else {
+      Prim q0, q1, q2, q3;
+      ld(ring + ((it + 1) % NS) * 5 * BAND, base, q0);
+      ld(ring + ((it + 2) % NS) * 5 * BAND, base, q1);
+      ld(ring + ((it + 3) % NS) * 5 * BAND, base, q2);
+      ld(ring + ((it + 4) % NS) * 5 * BAND, base, q3);
+      face_flux<2, SCH>(q0, q1, q2, q3, G, fz_out + w, Gm::FZ);
+    }
   };
   const int warp = tid >> 5, lane = tid & 31;
   // this thread's face tasks (the same on every plane): warp-uniform direction

@@ -52,6 +52,11 @@ def algorithmic_costs(nb=16, ng=4, fill_mode="gather"):
 
 
 FP64_INSTR_PER_CU = 1498.0
+# executed thread-instructions per cell-update of the two stage kernels (ncu
+# source page of the current kernels; profiles/r02_sass_mix_v16.txt) -- the
+# issue-slot view of the same kernels (context beside the fp64 roofline)
+EXEC_INSTR_PER_CU = 3758.0
+EXEC_INSTR_SOURCE = "profiles/r02_sass_mix_v16.txt"
 
 
 def measured_traffic():
@@ -657,6 +662,13 @@ def main():
                "kernel": "hydro_advance (stage_fused_kernel<16,1> + <16,2>)",
                "algorithmic_fp64_instr_per_cell_update": fp_instr, "units_per_launch": cu_local}
     primary, other = (roof_fp, roof_hbm) if roof_fp["frac"] >= roof_hbm["frac"] else (roof_hbm, roof_fp)
+    # issue slots: 148 SMs x 4 schedulers x 1 warp-instruction per cycle
+    issue_peak = 148 * 4 * pks.get("sm_max_mhz", 1965.0) * 1e6 * 32 / 1e12   # T thread-instructions/s
+    issue_ach = EXEC_INSTR_PER_CU * cu_local / (adv_ms / 1e3) / 1e12
+    roof_issue = {"bound": "issue", "achieved": issue_ach, "peak": issue_peak, "unit": "T thread-inst/s",
+                  "frac": issue_ach / issue_peak, "executed_instr_per_cell_update": EXEC_INSTR_PER_CU,
+                  "source": EXEC_INSTR_SOURCE,
+                  "note": "executed (not algorithmic) instructions: the advance is issue/latency bound"}
     step_hbm = (adv_bytes + fill_bytes) * value / world / 1e9
 
     # end to end through the public API with host buffers (the paper's model:
@@ -699,7 +711,7 @@ def main():
             "config": dict(workload_config(world), l2_flush="not needed: 2.2 GB state per GPU >> 126 MB L2",
                            kernel_variant=int(lib.orcha_get_kernel_variant()), fill_mode=fill_eff,
                            parallelism=f"blocks over {world} GPU(s)"),
-            "roofline": primary, "roofline_other": other,
+            "roofline": primary, "roofline_other": other, "roofline_issue": roof_issue,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
                                        "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},
             "advance_ms": adv_ms, "method": args.method, "dt_mode": args.dt_mode, "variants": variants,

@@ -180,8 +180,12 @@ struct Geo {
   static constexpr size_t SMEM =
       sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ + (ZC ? 5 * FZ : 0)) + 64 +
       ((NS * IR + 15) / 16) * 16;
-  // CTAs per SM we aim for: shared memory bound (227 KB per SM), at most 4
-  static constexpr int MINB_S = (int)(226000 / (SMEM + 1024));
+  // CTAs per SM we aim for: shared memory bound (228 KB per SM, 1 KB of it
+  // reserved per CTA), at most 8
+#ifndef ORCHA_SMEM_PER_SM
+#define ORCHA_SMEM_PER_SM 226000
+#endif
+  static constexpr int MINB_S = (int)(ORCHA_SMEM_PER_SM / (SMEM + 1024));
   static constexpr int MINB_R = 65536 / (NT * 80);  // at ~80 registers per thread
   static constexpr int MINB_SR = MINB_S < MINB_R ? MINB_S : MINB_R;
   static constexpr int MINB = MINB_SR < 1 ? 1 : (MINB_SR > 8 ? 8 : MINB_SR);

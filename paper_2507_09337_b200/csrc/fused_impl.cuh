@@ -95,6 +95,14 @@
 #ifndef ORCHA_ZCARRY
 #define ORCHA_ZCARRY 1
 #endif
+// x-face slope sharing (ORCHA_XSHFL): an x-face slot deals CELLS to lanes
+// (31 new ones per warp, one overlap lane); each lane computes its cell's
+// x-slope once, both face states q +- s/2, and takes the right state of its
+// face from the next lane (__shfl_down) -- one slope per x-face instead of two
+// (bitwise the same values)
+#ifndef ORCHA_XSHFL
+#define ORCHA_XSHFL 0
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 #ifndef ORCHA_ISSUE_LAST
 #define ORCHA_ISSUE_LAST 0
@@ -161,7 +169,9 @@ struct Geo {
   static constexpr int FZ = H * W;                           // z-faces per band (and cells)
   // face tasks are dealt out in warp-sized slots of one direction each; the
   // warp count is chosen so every warp gets two slots (two rounds)
-  static constexpr int SX = (FX + 31) / 32, SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
+  static constexpr int NCX = H * (W + 2);                    // x-slope cells per band plane (ORCHA_XSHFL)
+  static constexpr int SX = ORCHA_XSHFL ? (NCX - 1 + 30) / 31 : (FX + 31) / 32;
+  static constexpr int SY = (FY + 31) / 32, SZ = (FZ + 31) / 32;
   static constexpr int NSLOT = SX + SY + SZ;
   static constexpr int RQ = (STAGE == 1 || MODE == 1 || NB != 16) ? ORCHA_ROUNDS1 : ORCHA_ROUNDS2;  // face rounds per warp and plane
   static constexpr int NW8 = (NSLOT + ORCHA_ROUNDS8 - 1) / (ORCHA_ROUNDS8 > 0 ? ORCHA_ROUNDS8 : 1);
@@ -399,12 +409,28 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   };
   auto x_task = [&](int t, int base, int it) {
     const double* P = ring + ((it + 2) % NS) * 5 * BAND;
-    Prim q0, q1, q2, q3;
-    ld(P, base, q0);
-    ld(P, base + 1, q1);
-    ld(P, base + 2, q2);
-    ld(P, base + 3, q3);
-    face_flux<0, SCH>(q0, q1, q2, q3, G, Fx + t, Gm::FX);
+    if constexpr (ORCHA_XSHFL) {
+      // t = the face index this lane stores (-1: none); base = its cell's
+      // stencil (cells li-1 .. li+1); the whole warp runs this (shuffle)
+      Prim qm, q, qp, up, dn, R;
+      ld(P, base, qm);
+      ld(P, base + 1, q);
+      ld(P, base + 2, qp);
+      plm_cell<SCH>(qm, q, qp, G, &up, &dn);
+      R.r = __shfl_down_sync(0xffffffffu, dn.r, 1);
+      R.u = __shfl_down_sync(0xffffffffu, dn.u, 1);
+      R.v = __shfl_down_sync(0xffffffffu, dn.v, 1);
+      R.w = __shfl_down_sync(0xffffffffu, dn.w, 1);
+      R.p = __shfl_down_sync(0xffffffffu, dn.p, 1);
+      if (t >= 0) riemann_store<0, SCH>(up, R, G, Fx + t, Gm::FX);
+    } else {
+      Prim q0, q1, q2, q3;
+      ld(P, base, q0);
+      ld(P, base + 1, q1);
+      ld(P, base + 2, q2);
+      ld(P, base + 3, q3);
+      face_flux<0, SCH>(q0, q1, q2, q3, G, Fx + t, Gm::FX);
+    }
   };
   // y-face between band rows f-1 and f of column i
   auto y_task = [&](int u, int base, int it) {
@@ -462,12 +488,26 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   for (int r = 0; r < Gm::ROUNDS; r++) {
     const int m = r * Gm::NW + warp;
     int kind = 3, t = 0;
-    if (m < Gm::SX) { t = m * 32 + lane; kind = t < Gm::FX ? 0 : 3; }
+    int xbase = 0;
+    if (m < Gm::SX) {
+      if constexpr (ORCHA_XSHFL) {
+        // cell c of the band plane's rows of W+2 x-slope cells (output
+        // columns -1 .. W); every lane of the slot runs the task (shuffle)
+        const int c = m * 31 + lane, cc = c < Gm::NCX ? c : Gm::NCX - 1;
+        const int j = cc / (W + 2), u = cc - j * (W + 2);
+        kind = 0;
+        t = (c < Gm::NCX && lane < 31 && u <= W) ? j * (W + 1) + u : -1;
+        xbase = (j + 2) * IPX + (u - 2 - OFF + INO);
+      } else {
+        t = m * 32 + lane;
+        kind = t < Gm::FX ? 0 : 3;
+      }
+    }
     else if (m < Gm::SX + Gm::SY) { t = (m - Gm::SX) * 32 + lane; kind = t < Gm::FY ? 1 : 3; }
     else if (m < Gm::NSLOT) { t = (m - Gm::SX - Gm::SY) * 32 + lane; kind = t < Gm::FZ ? 2 : 3; }
     tkind[r] = kind;
     ttask[r] = t;
-    tbase[r] = kind < 3 ? task_base(kind, t) : 0;
+    tbase[r] = (ORCHA_XSHFL && kind == 0) ? xbase : kind < 3 ? task_base(kind, t) : 0;
   }
 
   bool writes_faces = false;

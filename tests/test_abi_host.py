@@ -164,3 +164,33 @@ def test_fnv1a64_reference_vectors(lib):
     assert hydro.fnv1a64(lib, b"foobar") == 0x85944171f73967e8
     # continuation: hashing in pieces == hashing the concatenation
     assert hydro.fnv1a64(lib, b"bar", hydro.fnv1a64(lib, b"foo")) == 0x85944171f73967e8
+
+
+def test_round2_entry_points_validate_arguments_without_device_work(lib):
+    # argument errors are synchronous and need no device (include/orcha.h)
+    rc, g = create(lib, desc())
+    assert rc == 0
+    E_ARG = -1
+    n = ctypes.c_void_p(0)
+    # unit entry points: null grid / buffers, n and dir out of range
+    assert lib.orcha_unit_eos(None, 1, n, n, n, n, n, None) == E_ARG
+    assert lib.orcha_unit_eos(g, -1, n, n, n, n, n, None) == E_ARG
+    assert lib.orcha_unit_eos(g, 4, None, n, n, n, n, None) == E_ARG
+    assert lib.orcha_unit_face_flux(g, 3, 4, n, n, None) == E_ARG
+    assert lib.orcha_unit_riemann(g, -1, 4, n, n, n, None) == E_ARG
+    assert lib.orcha_unit_riemann(g, 0, 0, None, None, None, None) == 0      # n = 0: nothing to do
+    # overlapped step, peer mode, push_dt, fill_prepare: null arguments
+    assert lib.orcha_hydro_step_overlap(None, None, None, None) == E_ARG
+    assert lib.orcha_comm_peer_register(None, None, None) == E_ARG
+    assert lib.orcha_comm_check(None) == E_ARG
+    assert lib.orcha_comm_push_dt(None, None, 0, None) == E_ARG
+    assert lib.orcha_fill_prepare(None, 0, None) == E_ARG
+    # instrumentation: too small an output array; the switch itself is host-only
+    ms = (ctypes.c_double * 3)()
+    assert lib.orcha_phase_times(ms, None, 3) == E_ARG
+    assert lib.orcha_set_phase_timing(0) == 0
+    assert lib.orcha_probe_fp64(0, None, None, None) == E_ARG
+    h = ctypes.c_uint64(0)
+    assert lib.orcha_fnv1a64(None, 4, ctypes.byref(h)) == E_ARG
+    assert "null" in lib.orcha_last_error().decode() or "orcha_fnv1a64" in lib.orcha_last_error().decode()
+    lib.orcha_grid_destroy(g)

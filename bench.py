@@ -359,9 +359,9 @@ def other_workloads(stream):
     (2D Sedov, 4x4 blocks of 8^2), configs[1] (Sod: 1D 64 blocks x 16 cells
     and the 2D tube of 64 x 1 blocks of 16^2), configs[2] (3D Sedov 128^3 as
     512 blocks of 16^3), and a large 2D Sedov (2048^2 as 128 x 128 blocks of
-    16^2) so the 2D kernels are measured at a size that fills the GPU.  1D/2D
-    grids run the reference kernels (one thread per output cell; the fused
-    kernels cover 3D 8^3/16^3/32^3 blocks, DESIGN.md d2)."""
+    16^2) so the 2D kernels are measured at a size that fills the GPU.  2D
+    grids of 8^2 / 16^2 blocks run the one-kernel 2D step (kernels_fused2d.cu),
+    1D grids the reference kernels (one thread per output cell)."""
     import numpy as np
     import torch
 
@@ -401,7 +401,10 @@ def other_workloads(stream):
         ms = a.elapsed_time(b) / c["steps"]
         cells = int(np.prod(N))
         out[name] = {"value": cells / (ms / 1e3), "unit": UNIT, "ms_per_step": ms, "cells": cells,
-                     "steps": c["steps"], "kernels": "fused" if nd == 3 else "reference (one thread per cell)"}
+                     "steps": c["steps"],
+                     "kernels": "fused z-marching (two stage kernels)" if nd == 3
+                     else "fused 2D (both stages in one kernel, U1 in shared memory)" if nd == 2 and c["nb"][0] in (8, 16)
+                     else "reference (one thread per cell)"}
         del pk, g
     return out
 

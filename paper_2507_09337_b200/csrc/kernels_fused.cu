@@ -22,6 +22,10 @@ ORCHA_FUSED_DECL(16, 1)
 ORCHA_FUSED_DECL(32, 0)
 ORCHA_FUSED_DECL(32, 1)
 
+bool fused2d_supported(const DevGrid& G);
+cudaError_t launch_advance_fused2d(const DevGrid& G, double* state, int nslots, const SlotInfo* slots,
+                                   const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
+                                   DevStatus* st, cudaStream_t s);
 cudaError_t launch_advance_ref(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                const double* d_dt, double h_dt, DtRecord* records, long long* nrecords,
                                DevStatus* st, cudaStream_t s);
@@ -48,6 +52,8 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
                                  DevStatus* st, cudaStream_t s, const PushEntry* push, const NbrEntry* nbr,
                                  bool push_x_only, int parts) {
   const int pk = push_x_only ? 2 : 1;
+  if (fused2d_supported(G) && parts == 3)  // 2D: both stages in one kernel, U1 on chip
+    return launch_advance_fused2d(G, state, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   if (!fused_supported(G))
     return launch_advance_ref(G, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s);
   // the F4 scheme variants (HLLC, MC, the expensive EOS) run their own instantiations (scheme 1)

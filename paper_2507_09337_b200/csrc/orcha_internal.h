@@ -209,7 +209,8 @@ class PhaseScope {
  private:
   int phase_;
   cudaStream_t stream_;
-  int idx_;
+  int idx_;                 // 0: this scope holds an event pair (a_, b_)
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
 };
 
 }  // namespace orcha

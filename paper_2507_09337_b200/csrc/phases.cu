@@ -26,11 +26,12 @@ struct Pair {
 };
 std::mutex g_mu;
 bool g_on = false;
-std::vector<Pair> g_live;   // recorded, not yet queried
+std::vector<Pair> g_live;   // recorded (both events), not yet queried
 std::vector<Pair> g_free;   // reusable event pairs
-std::vector<int> g_open;    // per phase: index into g_live of the open pair (-1 none)
 }  // namespace
 
+// The scope owns its event pair until it ends; only then does the pair join
+// the recorded list, so a query between the two records cannot mismatch it.
 PhaseScope::PhaseScope(int phase, cudaStream_t s) : phase_(phase), stream_(s), idx_(-1) {
   nvtxRangePushA(kPhaseName[phase]);
   std::lock_guard<std::mutex> lk(g_mu);
@@ -42,20 +43,22 @@ PhaseScope::PhaseScope(int phase, cudaStream_t s) : phase_(phase), stream_(s), i
   } else if (cudaEventCreate(&p.a) != cudaSuccess || cudaEventCreate(&p.b) != cudaSuccess) {
     return;
   }
-  p.phase = phase;
   if (cudaEventRecord(p.a, s) != cudaSuccess) {
     g_free.push_back(p);
     return;
   }
-  g_live.push_back(p);
-  idx_ = (int)g_live.size() - 1;
+  a_ = p.a;
+  b_ = p.b;
+  idx_ = 0;
 }
 
 PhaseScope::~PhaseScope() {
   nvtxRangePop();
   if (idx_ < 0) return;
   std::lock_guard<std::mutex> lk(g_mu);
-  if (idx_ < (int)g_live.size()) cudaEventRecord(g_live[idx_].b, stream_);
+  Pair p{phase_, a_, b_};
+  if (cudaEventRecord(p.b, stream_) == cudaSuccess) g_live.push_back(p);
+  else g_free.push_back(p);
 }
 
 }  // namespace orcha

@@ -431,6 +431,9 @@ def main():
     ap.add_argument("--dt-mode", default="device", choices=["device", "host"],
                     help="dt kept on the device (orcha_compute_dt_device, default) or returned to the host every step")
     ap.add_argument("--no-variants", action="store_true", help="skip the per-stage measurement beside the main line")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1: NCCL halo exchange + dt allgather (default), or the F2 peer mode over CUDA IPC "
+                         "(other ranks' packets read directly, device barriers; gloo carries only the handles)")
     ap.add_argument("--fill-mode", default="gather", choices=["gather", "full"],
                     help="guard fill: gather (x-guards only, y/z rows staged from their owners; default) or full")
     args = ap.parse_args()
@@ -452,12 +455,25 @@ def main():
         args.gpus = world
     if world not in GPU_GRIDS:
         raise SystemExit(f"--gpus must be one of {sorted(GPU_GRIDS)}")
+    # ORCHA_BENCH_SAME_GPU=1 (functional runs on a one-GPU box): every rank on
+    # GPU 0 -- only with --comm ipc (NCCL refuses two ranks on one GPU); the
+    # ranks then time-slice the GPU, so the numbers are not a scaling result
+    same_gpu = os.environ.get("ORCHA_BENCH_SAME_GPU") == "1" and world > 1
+    if same_gpu and args.comm != "ipc":
+        raise SystemExit("ORCHA_BENCH_SAME_GPU=1 needs --comm ipc")
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if args.comm == "ipc" else "nccl"
+    red_dev = "cpu" if backend == "gloo" else "cuda"   # device of the timing reductions
     if world > 1:
-        # NCCL's own communicator lines (ranks, channels, NVLS / P2P transport) on stderr
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            # NCCL's own communicator lines (ranks, channels, NVLS / P2P transport) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     if rank == 0 and not os.path.exists(abi.library_path(False)):
         build.build()
     if world > 1:
@@ -478,14 +494,24 @@ def main():
     bk = np.arange(BRICK_BLOCKS[2]) + rz * BRICK_BLOCKS[2]
     ids = ((bk[:, None, None] * nblk[1] + bj[None, :, None]) * nblk[0] + bi[None, None, :]).reshape(-1)
     comm = None
-    if world > 1:
-        comm = hydro.Comm.create(g, world, rank, hydro.brick_owner(nblk, BRICK_BLOCKS, GPU_GRIDS[world]))
+    owner = hydro.brick_owner(nblk, BRICK_BLOCKS, GPU_GRIDS[world])
+    if world > 1 and args.comm == "nccl":
+        comm = hydro.Comm.create(g, world, rank, owner)
     pk = hydro.Packet(g, ids)
     # initial Sedov state of this brick (host, closed form) -> pinned -> pack
     host = torch.from_numpy(inp.sedov_packet(N, NB, ids, xmax=(float(px), float(py), float(pz)))).pin_memory()
     stream = torch.cuda.current_stream()
     pk.pack(host, stream)
     stream.synchronize()
+    if world > 1 and args.comm == "ipc":
+        # F2 peer mode across processes: exchange the CUDA IPC blobs, map the
+        # other ranks' packets, counters and dt buffers; tables + kernels now
+        comm = hydro.Comm.create_ipc(g, world, rank, owner)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, comm.ipc_export(pk))
+        comm.ipc_attach(blobs)
+        hydro.orcha_fill_prepare([pk], comm)
+        torch.cuda.synchronize()
 
     adv_ev = []
 
@@ -530,7 +556,7 @@ def main():
             step(record=True, method=method)
         v1.record(stream)
         torch.cuda.synchronize()
-        vt = torch.tensor([v0.elapsed_time(v1) / nsteps], dtype=torch.float64, device="cuda")
+        vt = torch.tensor([v0.elapsed_time(v1) / nsteps], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(vt, op=dist.ReduceOp.MAX)
         vms = float(vt.item())
@@ -560,7 +586,7 @@ def main():
     launches = lib.orcha_launch_count() - launches0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -568,7 +594,7 @@ def main():
     value = cells / (ms / 1e3)
     adv_ms = statistics.mean(a.elapsed_time(b) for a, b in adv_ev)
     variants = {}
-    if args.method == "telescoped" and not args.no_variants:
+    if args.method == "telescoped" and not args.no_variants and args.comm != "ipc":
         # SURVEY 8(f) F1, measured beside the paper's telescoped step (same protocol)
         variants["per-stage"] = timed_variant("per-stage", args.steps)
         variants["per-stage"]["note"] = ("fill -> dt -> stage 1 (interior) -> U1 guard refill -> stage 2; "
@@ -627,7 +653,7 @@ def main():
                           "dt includes the allgather; gather fill mode on one GPU launches no fill kernel")
         busy = (phases["fill"] + phases["dt"] + phases["stage1"] + phases["stage2"]) / pms
         mine = torch.tensor([ms, adv_ms, busy, phases["exchange"], phases["dt_allgather"]], dtype=torch.float64,
-                            device="cuda")
+                            device=red_dev)
         if world > 1:
             allr = [torch.empty_like(mine) for _ in range(world)]
             dist.all_gather(allr, mine)
@@ -678,6 +704,8 @@ def main():
     # the packet is shipped H2D, advanced and shipped back every cycle)
     e2e = None
     e2e_serial = None
+    if args.comm == "ipc" and world > 1:
+        args.e2e_steps = 0   # peer mode takes one packet per rank; the streamed e2e uses 16
     if args.e2e_steps > 0:
         e2e = streamed_e2e(g, ids, N, px, py, pz, comm, stream, args.e2e_steps, args.e2e_packets, world,
                              copy_priority=args.e2e_priority, copy_streams=args.e2e_copy_streams)
@@ -695,7 +723,7 @@ def main():
         s1.record(stream)
         torch.cuda.synchronize()
         ems = s0.elapsed_time(s1) / args.e2e_steps
-        te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        te = torch.tensor([ems], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ems = float(te.item())
@@ -713,7 +741,9 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (closed-form Sedov IC)",
             "config": dict(workload_config(world), l2_flush="not needed: 2.2 GB state per GPU >> 126 MB L2",
                            kernel_variant=int(lib.orcha_get_kernel_variant()), fill_mode=fill_eff,
-                           parallelism=f"blocks over {world} GPU(s)"),
+                           parallelism=f"blocks over {world} GPU(s)",
+                           comm=(args.comm if world > 1 else None),
+                           same_gpu=(True if same_gpu else None)),
             "roofline": primary, "roofline_other": other, "roofline_issue": roof_issue,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
                                        "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},

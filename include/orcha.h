@@ -502,6 +502,25 @@ int32_t orcha_comm_peer_register(orcha_comm* comm, orcha_packet* packet, void* s
  * prepare every rank after all have registered, before the first step.
  * Errors: as orcha_fill_guardcells. */
 int32_t orcha_fill_prepare(orcha_packet* const* packets, int32_t npackets, orcha_comm* comm);
+/* F2 peer mode between PROCESSES (one per GPU of a node, or several sharing
+ * one GPU), no NCCL: orcha_comm_create_ipc makes rank `rank`'s communicator;
+ * orcha_comm_ipc_export writes this rank's blob -- CUDA IPC handles of its
+ * packet's state allocation (+ offset), its dt gather buffer and its barrier
+ * counter, and the packet's block ids (packet = ONE packet holding every
+ * block the rank owns; blob = NULL queries *size); the caller exchanges the
+ * blobs (e.g. torch.distributed all_gather over gloo) and passes all of them,
+ * in rank order, `stride` bytes apart, to orcha_comm_ipc_attach, which maps
+ * the other ranks' memory (cudaIpcOpenMemHandle with lazy peer access) and
+ * enters peer mode: from then on the calls behave exactly as for a LOCAL
+ * communicator in peer mode (above) -- direct reads of other ranks' rows,
+ * x-guard writes into them, device barriers over the mapped counters, the
+ * one-shot peer dt.  Call orcha_fill_prepare after attaching.
+ * Errors: ORCHA_E_ARG (bad blob, packet not holding exactly the rank's
+ * blocks), ORCHA_E_RANGE, ORCHA_E_STATE (call order), ORCHA_E_CUDA (IPC). */
+int32_t orcha_comm_create_ipc(const orcha_grid* grid, int32_t nranks, int32_t rank, const int32_t* block_owner,
+                              orcha_comm** out);
+int32_t orcha_comm_ipc_export(orcha_comm* comm, orcha_packet* packet, void* blob, size_t cap, size_t* size);
+int32_t orcha_comm_ipc_attach(orcha_comm* comm, const void* blobs, size_t stride);
 /* ORCHA_E_STATE if a peer barrier of this communicator timed out (device flag;
  * synchronizes), else ORCHA_OK. */
 int32_t orcha_comm_check(orcha_comm* comm);

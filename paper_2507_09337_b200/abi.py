@@ -36,7 +36,8 @@ EXPORTS = [
     "orcha_compute_dt_device", "orcha_unit_eos", "orcha_unit_face_flux", "orcha_unit_riemann",
     "orcha_comm_push_dt", "orcha_set_phase_timing", "orcha_phase_times", "orcha_probe_fp64",
     "orcha_fnv1a64", "orcha_comm_peer_register", "orcha_comm_check",
-    "orcha_fill_prepare", "orcha_hydro_step_overlap",
+    "orcha_fill_prepare", "orcha_hydro_step_overlap", "orcha_comm_create_ipc", "orcha_comm_ipc_export",
+    "orcha_comm_ipc_attach",
 ]
 
 
@@ -138,6 +139,9 @@ _SIGS = {
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),
     "orcha_set_phase_timing": (_i32, [_i32]),
     "orcha_phase_times": (_i32, [_P(_dbl), _P(_i64), _i32]),
+    "orcha_comm_create_ipc": (_i32, [_vp, _i32, _i32, _P(_i32), _P(_vp)]),
+    "orcha_comm_ipc_export": (_i32, [_vp, _vp, _vp, _sz, _P(_sz)]),
+    "orcha_comm_ipc_attach": (_i32, [_vp, _vp, _sz]),
     "orcha_hydro_step_overlap": (_i32, [_vp, _vp, _vp, _vp]),
     "orcha_fill_prepare": (_i32, [_P(_vp), _i32, _vp]),
     "orcha_comm_peer_register": (_i32, [_vp, _vp, _vp]),

@@ -19,6 +19,7 @@
 // so liborcha.so has no link-time NCCL dependency.  A LOCAL transport (virtual
 // ranks on one device, device-to-device copies) runs the same plan, pack and
 // unpack kernels without NCCL for tests.
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -276,6 +277,13 @@ struct orcha_comm {
   unsigned long long** d_ctr_ptrs = nullptr;  // device array: every rank's barrier counter
   unsigned long long bar_epoch = 0;           // barriers this rank has entered
   int* d_err = nullptr;                       // device flag: a peer barrier timed out
+  std::vector<void*> peer_gather;             // every rank's dt gather buffer (index = rank)
+  // F2 peer mode across processes (CUDA IPC; orcha_comm_create_ipc)
+  bool ipc = false;
+  unsigned long long* d_my_ctr = nullptr;     // this rank's barrier counter (exported)
+  orcha_packet* own_packet = nullptr;         // the packet this rank exported
+  std::vector<void*> ipc_mapped;              // opened peer allocations (closed on destroy)
+  std::vector<orcha_packet*> shadow;          // other ranks' packets: their mapped state + ids (owned)
 };
 
 namespace orcha {
@@ -388,10 +396,12 @@ static void free_plan(CommPlan* P) {
 
 void comm_drop_packet(orcha_packet* p) {
   std::lock_guard<std::mutex> lk(g_comm_mu);
-  for (auto* c : g_comms)
+  for (auto* c : g_comms) {
     if (c->hub)
       for (auto*& q : c->hub->peer_packet)
         if (q == p) q = nullptr;  // peer mode: the rank must register a packet again
+    if (c->own_packet == p) c->own_packet = nullptr;
+  }
   for (auto* c : g_comms)
     for (size_t i = 0; i < c->plans.size();) {
       bool hit = false;
@@ -462,9 +472,11 @@ static int32_t gather_records(orcha_comm* c, const void* mine, cudaStream_t s) {
   if (c->peer_mode) {
     // F2: one-shot P2P -- this rank's record into slot `rank` of every rank's
     // gather buffer, then a device barrier: every slot is then filled
-    for (auto* m : c->hub->members) {
-      if (!m) return fail(ORCHA_E_STATE, "peer mode: a member rank was destroyed");
-      e = cudaMemcpyAsync((char*)m->d_gather + 32 + 32 * (size_t)c->rank, base, 32, cudaMemcpyDeviceToDevice, s);
+    for (int q = 0; q < c->nranks; q++) {
+      void* g = (q < (int)c->peer_gather.size()) ? c->peer_gather[q] : nullptr;
+      if (c->hub && (!c->hub->members[q])) g = nullptr;
+      if (!g) return fail(ORCHA_E_STATE, "peer mode: rank " + std::to_string(q) + " is gone");
+      e = cudaMemcpyAsync((char*)g + 32 + 32 * (size_t)c->rank, base, 32, cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return cuda_fail(e, "dt record push (peer mode)");
     }
     return comm_peer_barrier(c, s);
@@ -586,6 +598,10 @@ int comm_rank(const orcha_comm* c) { return c->rank; }
 int32_t comm_peer_packets(const orcha_comm* c, std::vector<orcha_packet*>* out) {
   out->clear();
   if (!c->peer_mode) return fail(ORCHA_E_STATE, "not in peer mode");
+  if (c->ipc) {
+    *out = c->shadow;
+    return ORCHA_OK;
+  }
   for (int q = 0; q < c->nranks; q++) {
     orcha_packet* p = c->hub->peer_packet[q];
     if (!p) return fail(ORCHA_E_STATE, "peer mode: rank " + std::to_string(q) + " has not registered its packet");
@@ -595,6 +611,9 @@ int32_t comm_peer_packets(const orcha_comm* c, std::vector<orcha_packet*>* out) 
 }
 
 static void destroy_comm(orcha_comm* c) {
+  for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+  for (auto* p : c->shadow) delete p;
+  cudaFree(c->d_my_ctr);
   for (auto* p : c->plans) free_plan(p);
   for (auto& b : c->bufs) { cudaFree(b.d_send); cudaFree(b.d_recv); }
   cudaFree(c->d_gather);
@@ -766,6 +785,9 @@ extern "C" int32_t orcha_comm_peer_register(orcha_comm* c, orcha_packet* p, void
   cudaError_t e = cudaFuncGetAttributes(&fa, peer_barrier_kernel);
   if (e != cudaSuccess) return cuda_fail(e, "load peer barrier kernel");
   hub->peer_packet[c->rank] = p;
+  c->peer_gather.assign(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; q++)
+    if (hub->members[q]) c->peer_gather[q] = hub->members[q]->d_gather;
   c->peer_mode = true;
   return ORCHA_OK;
 }
@@ -777,5 +799,152 @@ extern "C" int32_t orcha_comm_check(orcha_comm* c) {
   cudaError_t e = cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "read peer barrier flag");
   if (err) return fail(ORCHA_E_STATE, "a peer barrier timed out (a rank never arrived)");
+  return ORCHA_OK;
+}
+
+// ----------------------------------------------- F2 peer mode over CUDA IPC ---
+// The same peer mode between PROCESSES (one per GPU on a node, or several on
+// one GPU): each rank exports its packet state, dt gather buffer and barrier
+// counter as CUDA IPC handles in a blob, the caller exchanges the blobs
+// (e.g. torch.distributed over gloo), and every rank maps the others' memory
+// (cudaIpcOpenMemHandle, peer access over NVLink between GPUs).  The other
+// ranks' packets become "shadow" packets (their mapped state and block ids)
+// that the fill plan addresses like the LOCAL transport's.
+namespace orcha {
+namespace {
+constexpr uint32_t kIpcMagic = 0x5049524fu;  // "ORIP"
+struct IpcHeader {
+  uint32_t magic;
+  int32_t rank, nranks, nslots;
+  uint64_t state_off;
+  cudaIpcMemHandle_t h_state, h_gather, h_ctr;
+};
+// base of the allocation holding p (the torch caching allocator sub-allocates)
+cudaError_t alloc_base(void* p, void** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (Fn)f;
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  *base = (void*)b;
+  return cudaSuccess;
+}
+}  // namespace
+}  // namespace orcha
+
+extern "C" int32_t orcha_comm_create_ipc(const orcha_grid* g, int32_t nranks, int32_t rank, const int32_t* owner,
+                                         orcha_comm** out) {
+  if (!out) return fail(ORCHA_E_ARG, "null argument");
+  *out = nullptr;
+  int32_t rc = validate_owner(g, nranks, owner);
+  if (rc) return rc;
+  if (rank < 0 || rank >= nranks) return fail(ORCHA_E_ARG, "rank out of range");
+  orcha_comm* c = new orcha_comm();
+  c->grid = g;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->owner.assign(owner, owner + g->nblocks);
+  c->local = false;
+  c->ipc = true;
+  cudaError_t e = cudaMalloc(&c->d_gather, 32 * (size_t)(nranks + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_my_ctr, 256);
+  if (e == cudaSuccess) e = cudaMemset(c->d_my_ctr, 0, 256);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    destroy_comm(c);
+    return cuda_fail(e, "allocate IPC communicator buffers");
+  }
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  g_comms.push_back(c);
+  *out = c;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_comm_ipc_export(orcha_comm* c, orcha_packet* p, void* blob, size_t cap, size_t* size) {
+  if (!c || !p || !size) return fail(ORCHA_E_ARG, "null argument");
+  if (!c->ipc) return fail(ORCHA_E_ARG, "orcha_comm_ipc_export needs an orcha_comm_create_ipc communicator");
+  if (p->grid != c->grid) return fail(ORCHA_E_ARG, "packet of another grid");
+  long long owned = 0;
+  for (long long b = 0; b < c->grid->nblocks; b++) owned += c->owner[b] == c->rank;
+  for (long long b : p->ids)
+    if (c->owner[b] != c->rank) return fail(ORCHA_E_RANGE, "packet holds a block this rank does not own");
+  if ((long long)p->ids.size() != owned)
+    return fail(ORCHA_E_ARG, "peer mode needs ONE packet per rank holding every block the rank owns");
+  *size = sizeof(IpcHeader) + sizeof(int64_t) * p->ids.size();
+  if (!blob) return ORCHA_OK;
+  if (cap < *size) return fail(ORCHA_E_ARG, "blob buffer too small");
+  IpcHeader h;
+  memset(&h, 0, sizeof h);
+  h.magic = kIpcMagic;
+  h.rank = c->rank;
+  h.nranks = c->nranks;
+  h.nslots = p->nslots;
+  void* base = nullptr;
+  cudaError_t e = alloc_base(p->state, &base);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_state, base);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_gather, c->d_gather);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_ctr, c->d_my_ctr);
+  if (e != cudaSuccess) return cuda_fail(e, "IPC export");
+  h.state_off = (uint64_t)((char*)p->state - (char*)base);
+  memcpy(blob, &h, sizeof h);
+  memcpy((char*)blob + sizeof h, p->ids.data(), sizeof(int64_t) * p->ids.size());
+  c->own_packet = p;
+  return ORCHA_OK;
+}
+
+extern "C" int32_t orcha_comm_ipc_attach(orcha_comm* c, const void* blobs, size_t stride) {
+  if (!c || !blobs) return fail(ORCHA_E_ARG, "null argument");
+  if (!c->ipc || !c->own_packet) return fail(ORCHA_E_STATE, "orcha_comm_ipc_export first");
+  if (c->peer_mode) return fail(ORCHA_E_STATE, "already attached");
+  std::vector<unsigned long long*> ctr(c->nranks, nullptr);
+  c->peer_gather.assign(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; q++) {
+    const char* b = (const char*)blobs + stride * (size_t)q;
+    IpcHeader h;
+    memcpy(&h, b, sizeof h);
+    if (h.magic != kIpcMagic || h.rank != q || h.nranks != c->nranks || h.nslots < 1 ||
+        sizeof h + sizeof(int64_t) * (size_t)h.nslots > stride)
+      return fail(ORCHA_E_ARG, "IPC blob " + std::to_string(q) + " is malformed or out of rank order");
+    if (q == c->rank) {
+      ctr[q] = c->d_my_ctr;
+      c->peer_gather[q] = c->d_gather;
+      continue;
+    }
+    std::vector<long long> ids((size_t)h.nslots);
+    memcpy(ids.data(), b + sizeof h, sizeof(int64_t) * ids.size());
+    for (long long id : ids)
+      if (id < 0 || id >= c->grid->nblocks || c->owner[id] != q)
+        return fail(ORCHA_E_RANGE, "IPC blob " + std::to_string(q) + " lists a block that rank does not own");
+    void *st = nullptr, *ga = nullptr, *ct = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&st, h.h_state, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) { c->ipc_mapped.push_back(st); e = cudaIpcOpenMemHandle(&ga, h.h_gather, cudaIpcMemLazyEnablePeerAccess); }
+    if (e == cudaSuccess) { c->ipc_mapped.push_back(ga); e = cudaIpcOpenMemHandle(&ct, h.h_ctr, cudaIpcMemLazyEnablePeerAccess); }
+    if (e != cudaSuccess) return cuda_fail(e, "IPC open");
+    c->ipc_mapped.push_back(ct);
+    orcha_packet* sh = new orcha_packet();  // a source only: never filled, advanced or destroyed by the caller
+    sh->grid = c->grid;
+    sh->nslots = h.nslots;
+    sh->ids = ids;
+    sh->state = (double*)((char*)st + h.state_off);
+    sh->scratch = nullptr;
+    c->shadow.push_back(sh);
+    ctr[q] = (unsigned long long*)ct;
+    c->peer_gather[q] = ga;
+  }
+  cudaError_t e = cudaMalloc(&c->d_ctr_ptrs, sizeof(void*) * c->nranks);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_ctr_ptrs, ctr.data(), sizeof(void*) * c->nranks, cudaMemcpyHostToDevice);
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, peer_barrier_kernel);
+  if (e != cudaSuccess) return cuda_fail(e, "IPC barrier tables");
+  c->peer_mode = true;
   return ORCHA_OK;
 }

@@ -609,7 +609,7 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
         for (int q2 = 0; q2 < next; q2++) {
           orcha_packet* sp = pk[q2];
           if (e.src >= sp->state && e.src < sp->state + (long long)sp->nslots * kNVar * G.cube) {
-            e.src = sp->scratch + (e.src - sp->state);
+            e.src = sp->scratch ? sp->scratch + (e.src - sp->state) : nullptr;  // IPC shadows: no stage-1 buffer
             break;
           }
         }
@@ -667,7 +667,7 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
         for (int q2 = 0; q2 < next; q2++) {
           orcha_packet* sp = pk[q2];
           if (e.dst >= sp->state && e.dst < sp->state + (long long)sp->nslots * kNVar * G.cube) {
-            e.dst = sp->scratch + (e.dst - sp->state);
+            e.dst = sp->scratch ? sp->scratch + (e.dst - sp->state) : nullptr;
             break;
           }
         }

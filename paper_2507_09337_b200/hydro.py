@@ -190,6 +190,29 @@ class Comm:
                  owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), hs)
         return [Comm(grid, ctypes.c_void_p(hs[r]), nranks, r, owner) for r in range(nranks)]
 
+    @staticmethod
+    def create_ipc(grid: Grid, nranks: int, rank: int, owner) -> "Comm":
+        """F2 peer mode across processes (CUDA IPC; no NCCL): export, exchange, attach."""
+        owner = np.ascontiguousarray(owner, dtype=np.int32)
+        h = ctypes.c_void_p()
+        abi.call(grid.lib, "orcha_comm_create_ipc", grid.handle, nranks, rank,
+                 owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(h))
+        return Comm(grid, h, nranks, rank, owner)
+
+    def ipc_export(self, packet) -> bytes:
+        n = ctypes.c_size_t()
+        abi.call(self.lib, "orcha_comm_ipc_export", self.handle, packet.handle, None, 0, ctypes.byref(n))
+        buf = ctypes.create_string_buffer(n.value)
+        abi.call(self.lib, "orcha_comm_ipc_export", self.handle, packet.handle, buf, n.value, ctypes.byref(n))
+        return buf.raw[:n.value]
+
+    def ipc_attach(self, blobs) -> None:
+        """blobs: every rank's export, in rank order."""
+        stride = max(len(b) for b in blobs)
+        raw = b"".join(b.ljust(stride, b"\0") for b in blobs)
+        buf = ctypes.create_string_buffer(raw, len(raw))
+        abi.call(self.lib, "orcha_comm_ipc_attach", self.handle, buf, stride)
+
     def push(self, packets, stream=None, buffer: int = 0):
         arr, n = _handles(packets)
         abi.call(self.lib, "orcha_comm_push", self.handle, arr, n, int(buffer), ctypes.c_void_p(_stream_ptr(stream)))

@@ -489,8 +489,10 @@ int32_t orcha_hydro_step_overlap(orcha_packet* packet, orcha_comm* comm, orcha_d
  * serialising two ranks would wait forever at the first barrier -- and
  * time out), and must not allocate device memory between the ranks'
  * launches (CUDA's implicit synchronisation would serialise the streams):
- * call orcha_fill_prepare for every rank first.  Available for LOCAL (virtual-rank) communicators, whose
- * packets are directly addressable in one process (same-device "peers").
+ * call orcha_fill_prepare for every rank first.  orcha_comm_peer_register is
+ * for LOCAL (virtual-rank) communicators, whose packets are directly
+ * addressable in one process (same-device "peers"); across processes the CUDA
+ * IPC communicator below enters the same mode (orcha_comm_ipc_attach).
  * Errors: ORCHA_E_ARG (NCCL communicator, packet of another grid, packet not
  * holding exactly the rank's blocks), ORCHA_E_RANGE, ORCHA_E_CUDA. */
 int32_t orcha_comm_peer_register(orcha_comm* comm, orcha_packet* packet, void* stream);

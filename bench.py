@@ -129,7 +129,7 @@ def workload_config(world):
     return {"workload": "cfg4: 3D Sedov, 4096 blocks of 16^3 (+4 guards) per GPU, one packet",
             "global_cells": [nblk[a] * NB[a] for a in range(3)],
             "blocks_per_gpu": BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2], "gpu_grid": list(GPU_GRIDS[world]),
-            "ng": 4, "gamma": 1.4, "cfl": 0.4, "global_batch": None, "seq_len": None}
+            "ng": 4, "gamma": 1.4, "cfl": 0.4}
 
 
 def run_reference(args, rank, world):

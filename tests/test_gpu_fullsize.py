@@ -111,3 +111,50 @@ def test_cfg3_ten_steps_against_oracle(oracle_cfg3, parity):
             assert abs(dt - odt) <= 1e-13 * odt
         assert H.parity_error(out, O_) <= 1e-12, H.error_report(out, O_)
     assert pk.counters() == (0, -1)
+
+
+def test_cfg4_sedov_to_t005_matches_the_similarity_solution():
+    # BASELINE configs[3]'s full single-GPU size run to t = 0.05 through the
+    # bench's launch configuration (device dt, fused kernels, gather fill):
+    # properties that hold at any size (north_star) -- the shock
+    # radius within 2 dx of xi0 (E t^2/rho)^(1/5) = 0.3116 (xi0 = 1.032777,
+    # tests/exact/sedov.py), mass and energy conserved while the shock is
+    # inside the box, octant mirror symmetry to round-off, no floor hits
+    from paper_2507_09337_b200 import hydro
+    from tests.exact import sedov
+    g = H.make_grid(3, NB, NBLK)
+    ids = np.arange(g.nblocks)
+    pk = hydro.Packet(g, ids)
+    U0 = inp.sedov_packet(N, NB, ids)
+    pk.pack(U0)
+    clock = hydro.DevClock(0.0, 0.05)
+    steps = 0
+    while True:  # chunks of device-dt steps (no host sync inside a chunk)
+        for _ in range(100):
+            hydro.orcha_fill_guardcells([pk])
+            hydro.orcha_compute_dt_device([pk], clock)
+            hydro.orcha_hydro_advance_devdt(pk, clock.dt_tensor)
+        steps += 100
+        c = clock.read()
+        if c.t >= 0.05 or steps > 20000:
+            break
+    # steps after t_end have dt = 0 and leave the state bitwise unchanged
+    assert c.t == 0.05 and c.tag == 1
+    out = H.gather(g, [pk])
+    dx = 1.0 / N[0]
+    rho = out[0]
+    xc = (np.arange(N[0]) + 0.5) * dx - 0.5
+    r2 = xc[None, None, :] ** 2 + xc[None, :, None] ** 2 + xc[:, None, None] ** 2
+    b = (np.sqrt(r2) / dx).astype(int).ravel()
+    mean = np.bincount(b, rho.ravel()) / np.bincount(b)
+    R = (np.argmax(mean) + 0.5) * dx
+    assert abs(R - sedov.shock_radius(0.05, 3)) <= 2 * dx, R
+    assert abs(rho.sum() * dx ** 3 - 1.0) <= 1e-12
+    E0 = inp.sedov(N)[4].sum()
+    assert abs(out[4].sum() - E0) <= 1e-12 * E0
+    for d in range(3):
+        ax = 3 - d
+        M = np.flip(out, axis=ax).copy()
+        M[1 + d] = -M[1 + d]
+        assert H.parity_error(out, M) <= 1e-12, d
+    assert pk.counters() == (0, -1)

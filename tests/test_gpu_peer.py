@@ -101,6 +101,20 @@ def test_peer_mode_bitwise_equal_single_domain(case):
     assert launches[-1] == 7 * n, launches
 
 
+@pytest.mark.parametrize("scheme", [(1, 0), (1, 1)])
+def test_peer_mode_with_scheme_variants(scheme):
+    # the F4 variants (HLLC, MC: the scheme-1 instantiations) through peer mode
+    from paper_2507_09337_b200 import hydro
+    ndim, nb, nblk, bc, gg, brick = CASES[1]
+    g = H.make_grid(ndim, nb, nblk, bc=bc, riemann=scheme[0], limiter=scheme[1])
+    owner = hydro.brick_owner(nblk, brick, gg)
+    U0 = inp.supersonic_field(g.N, seed=73)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
+    B, logB, _ = _run_peer(g, U0, owner, 4)
+    assert logB == [tuple(x) for x in logA]
+    assert np.array_equal(A, B)
+
+
 def test_peer_mode_scattered_owner_map():
     from paper_2507_09337_b200 import hydro  # noqa: F401
     g = H.make_grid(3, (8, 8, 8), (4, 3, 2), bc=((R, O), (P, P), (O, R)))

@@ -257,15 +257,37 @@ def streamed_loop(g, ids, N, px, py, pz, comm, stream, K, copy_priority=0, copy_
     d2hs = [torch.cuda.Stream(priority=copy_priority) for _ in range(copy_streams)]
     done = [None] * len(pks)
 
-    # one rank: each slab's dt records right after its pack, its guard fill
-    # right after the next slab's pack (the brick's z faces are outflow, so a
-    # z-slab's guards read only its two neighbour slabs) -- only the last
-    # slab's fill and the dt reduction stay between the last H2D and the
-    # first advance.  Several ranks: the set-wide fill with its exchange.
+    # one rank (lagged pipeline): the dt of a step is reduced on the device
+    # at the end of the previous step, from the records its stage-2 epilogues
+    # left (the values shipped out and back are bitwise the ones those
+    # epilogues saw); each slab's guard fill follows the next slab's pack
+    # (the brick's z faces are outflow, so a z-slab's guards read only its
+    # two neighbour slabs) and its advance + unpack follow the fill of the
+    # slab after it (which still reads its U^n): the first unpack of a step
+    # starts three slabs into the H2D chain.  Several ranks: the set-wide
+    # fill with its exchange, dt, then the advances.
     pipelined = comm is None
     clock = hydro.DevClock(0.0, math.inf)
 
+    def advance_out(i):
+        hydro.orcha_hydro_advance_devdt(pks[i], clock.dt_tensor, stream)
+        e = torch.cuda.Event()
+        e.record(stream)
+        d2h = d2hs[i % len(d2hs)]
+        d2h.wait_event(e)
+        pks[i].unpack(mesh[i], d2h, sync=False)
+        e2 = torch.cuda.Event()
+        e2.record(d2h)
+        done[i] = e2
+
+    def prime():
+        """Before the first step: upload the mesh once and reduce the first dt."""
+        for i, p in enumerate(pks):
+            p.pack(mesh[i], stream)
+        hydro.orcha_compute_dt_device(pks, clock, comm, stream)
+
     def one():
+        K_ = len(pks)
         ev_in = []
         for i, p in enumerate(pks):
             h2d = h2ds[i % len(h2ds)]
@@ -277,26 +299,23 @@ def streamed_loop(g, ids, N, px, py, pz, comm, stream, K, copy_priority=0, copy_
             ev_in.append(e)
             if pipelined:
                 stream.wait_event(e)
-                hydro.orcha_packet_dt_records(p, stream)
                 if i >= 1:
                     hydro.orcha_fill_guardcells_packet(pks, i - 1, stream)
+                if i >= 2:
+                    advance_out(i - 2)
         if pipelined:
-            hydro.orcha_fill_guardcells_packet(pks, len(pks) - 1, stream)
-        else:
-            for e in ev_in:
-                stream.wait_event(e)
-            hydro.orcha_fill_guardcells(pks, comm, stream)
+            hydro.orcha_fill_guardcells_packet(pks, K_ - 1, stream)
+            for i in range(max(K_ - 2, 0), K_):
+                advance_out(i)
+            hydro.orcha_compute_dt_device(pks, clock, comm, stream)  # the next step's dt, on the device
+            return
+        for e in ev_in:
+            stream.wait_event(e)
+        hydro.orcha_fill_guardcells(pks, comm, stream)
         hydro.orcha_compute_dt_device(pks, clock, comm, stream)  # dt stays on the device
-        for i, p in enumerate(pks):
-            hydro.orcha_hydro_advance_devdt(p, clock.dt_tensor, stream)
-            e = torch.cuda.Event()
-            e.record(stream)
-            d2h = d2hs[i % len(d2hs)]
-            d2h.wait_event(e)
-            p.unpack(mesh[i], d2h, sync=False)
-            e2 = torch.cuda.Event()
-            e2.record(d2h)
-            done[i] = e2
+        for i in range(K_):
+            advance_out(i)
+    one.prime = prime
     return pks, mesh, one, done
 
 
@@ -314,6 +333,9 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
     import torch.distributed as dist
 
     pks, mesh, one, done = streamed_loop(g, ids, N, px, py, pz, comm, stream, K, copy_priority, copy_streams)
+    if comm is None:
+        one.prime()
+        torch.cuda.synchronize()
     one()
     torch.cuda.synchronize()
     if world > 1:
@@ -348,8 +370,10 @@ def streamed_e2e(g, ids, N, px, py, pz, comm, stream, nsteps, K, world, copy_pri
                             "measured over the same pinned mesh buffers; the rest is the serial part of the step (last slab's H2D, fill, "
                             "dt, first slab's advance + D2H)"},
            "note": f"host-resident mesh, {len(mesh)} z-slab packets per GPU shipped in and out every step on copy "
-                   "streams overlapping the other packets' compute (each slab's dt records and guard fill as soon "
-                   "as it and its neighbours are on the device); step n+1 reads step n's output from the host"}
+                   "streams overlapping the other packets' compute (one rank: each slab's guard fill as soon as its "
+                   "neighbours are on the device, its advance and unpack right after the next slab's fill, the "
+                   "step's dt reduced on the device at the end of the previous step from its stage-2 records); "
+                   "step n+1 reads step n's output from the host"}
     return out
 
 

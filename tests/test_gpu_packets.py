@@ -159,3 +159,39 @@ def test_per_packet_fill_arguments():
     for bad in (-1, len(pks)):
         with pytest.raises(abi.OrchaError, match="ORCHA_E_ARG"):
             hydro.orcha_fill_guardcells_packet(pks, bad)
+
+
+@pytest.mark.parametrize("parity", [False, True])
+def test_bench_streamed_loop_equals_resident_run_and_oracle(parity):
+    # bench.py's own e2e loop (streamed_loop: the lagged pipeline -- each
+    # slab's fill after the next slab's pack, its advance + unpack after the
+    # following fill, the step's dt reduced at the end of the previous step
+    # from the stage-2 records) on a 16^3-block grid of 4 z-slabs: the host
+    # mesh after 4 steps is bitwise the device-resident run (and, parity
+    # build, the oracle), with the same dt every step
+    import math
+    import sys
+    import torch
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2507_09337_b200 import hydro
+    g = H.make_grid(3, (16, 16, 16), (2, 2, 4), parity=parity)
+    N = g.N
+    ids = np.arange(g.nblocks)
+    U0 = inp.sedov(N)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
+    s = torch.cuda.current_stream()
+    pks, mesh, one, done = bench.streamed_loop(g, ids, N, 1, 1, 1, None, s, 4, copy_priority=-1, copy_streams=2)
+    one.prime()
+    torch.cuda.synchronize()
+    for _ in range(4):
+        one()
+    torch.cuda.synchronize()
+    out = None
+    for p, m in zip(pks, mesh):
+        out = inp.from_blocks(m.numpy(), N, g.nb, p.block_ids, out)
+    assert np.array_equal(out, A)
+    if parity:
+        Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4)
+        assert np.array_equal(out, Oo)

@@ -816,8 +816,10 @@ constexpr uint32_t kIpcMagic = 0x5049524fu;  // "ORIP"
 struct IpcHeader {
   uint32_t magic;
   int32_t rank, nranks, nslots;
-  uint64_t state_off;
-  cudaIpcMemHandle_t h_state, h_gather, h_ctr;
+  uint64_t state_off, scratch_off;
+  int32_t scratch_in_state_alloc;  // the stage-1 buffer lives in the state's allocation
+  int32_t pad;
+  cudaIpcMemHandle_t h_state, h_scratch, h_gather, h_ctr;
 };
 // base of the allocation holding p (the torch caching allocator sub-allocates)
 cudaError_t alloc_base(void* p, void** base) {
@@ -888,13 +890,17 @@ extern "C" int32_t orcha_comm_ipc_export(orcha_comm* c, orcha_packet* p, void* b
   h.rank = c->rank;
   h.nranks = c->nranks;
   h.nslots = p->nslots;
-  void* base = nullptr;
+  void *base = nullptr, *sbase = nullptr;
   cudaError_t e = alloc_base(p->state, &base);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_state, base);
+  if (e == cudaSuccess) e = alloc_base(p->scratch, &sbase);  // the stage-1 buffer (per-stage variant)
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_scratch, sbase);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_gather, c->d_gather);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h.h_ctr, c->d_my_ctr);
   if (e != cudaSuccess) return cuda_fail(e, "IPC export");
   h.state_off = (uint64_t)((char*)p->state - (char*)base);
+  h.scratch_off = (uint64_t)((char*)p->scratch - (char*)sbase);
+  h.scratch_in_state_alloc = sbase == base ? 1 : 0;
   memcpy(blob, &h, sizeof h);
   memcpy((char*)blob + sizeof h, p->ids.data(), sizeof(int64_t) * p->ids.size());
   c->own_packet = p;
@@ -924,10 +930,22 @@ extern "C" int32_t orcha_comm_ipc_attach(orcha_comm* c, const void* blobs, size_
     for (long long id : ids)
       if (id < 0 || id >= c->grid->nblocks || c->owner[id] != q)
         return fail(ORCHA_E_RANGE, "IPC blob " + std::to_string(q) + " lists a block that rank does not own");
-    void *st = nullptr, *ga = nullptr, *ct = nullptr;
+    void *st = nullptr, *sc = nullptr, *ga = nullptr, *ct = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&st, h.h_state, cudaIpcMemLazyEnablePeerAccess);
-    if (e == cudaSuccess) { c->ipc_mapped.push_back(st); e = cudaIpcOpenMemHandle(&ga, h.h_gather, cudaIpcMemLazyEnablePeerAccess); }
-    if (e == cudaSuccess) { c->ipc_mapped.push_back(ga); e = cudaIpcOpenMemHandle(&ct, h.h_ctr, cudaIpcMemLazyEnablePeerAccess); }
+    if (e == cudaSuccess) c->ipc_mapped.push_back(st);
+    // the state and the stage-1 buffer may be sub-allocations of one
+    // allocation (the torch caching allocator): one handle, mapped once
+    if (e == cudaSuccess) {
+      if (h.scratch_in_state_alloc) {
+        sc = st;
+      } else {
+        e = cudaIpcOpenMemHandle(&sc, h.h_scratch, cudaIpcMemLazyEnablePeerAccess);
+        if (e == cudaSuccess) c->ipc_mapped.push_back(sc);
+      }
+    }
+    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&ga, h.h_gather, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) c->ipc_mapped.push_back(ga);
+    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&ct, h.h_ctr, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return cuda_fail(e, "IPC open");
     c->ipc_mapped.push_back(ct);
     orcha_packet* sh = new orcha_packet();  // a source only: never filled, advanced or destroyed by the caller
@@ -935,7 +953,7 @@ extern "C" int32_t orcha_comm_ipc_attach(orcha_comm* c, const void* blobs, size_
     sh->nslots = h.nslots;
     sh->ids = ids;
     sh->state = (double*)((char*)st + h.state_off);
-    sh->scratch = nullptr;
+    sh->scratch = (double*)((char*)sc + h.scratch_off);
     c->shadow.push_back(sh);
     ctr[q] = (unsigned long long*)ct;
     c->peer_gather[q] = ga;

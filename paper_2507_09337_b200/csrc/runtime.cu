@@ -816,24 +816,26 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
   const DevGrid& G0 = pk[0]->grid->dev;
   const bool xonly = buffer == 0 && npk == 1 && !push_enabled() && fill_mode() == 1 &&
                      kernel_variant() == 1 && fused_supported(G0);
-  if (f->peer) {
-    // F2 peer mode: the gather fill only (x-guards; stage 1 stages y/z rows
-    // from the owners, other ranks' included, and stage 2 pushes x-guards
-    // into them); the telescoped method only
-    if (!xonly || only >= 0)
-      return fail(ORCHA_E_STATE, "peer mode needs the gather fill (fill mode 1, fused kernels, one packet, no "
-                                 "guard push) and the telescoped method");
-    if (!(pk[0]->xguards_pushed && pk[0]->push_plan == f)) {
-      // after a pack: the x-guard fill reads other ranks' interiors, so every
-      // rank's pack must be done (device barrier)
-      rc = comm_peer_barrier(f->peer, s);
-      if (rc) return rc;
-    }
-  }
   // per-stage stage-1 buffer in gather mode: stage 1 wrote the U1 x-guards
   // (same plan), stage 2 stages the y/z rows of U1 from their owners
   const bool xonly_u1 = buffer == 1 && npk == 1 && !push_enabled() && fill_mode() == 1 && kernel_variant() == 1 &&
                         fused_supported(G0) && pk[0]->u1_xpushed && pk[0]->push_plan == f;
+  if (f->peer) {
+    // F2 peer mode: the gather fills only (x-guards; the stage kernels stage
+    // y/z rows from the owners, other ranks' included, and push x-guards into
+    // them) -- the telescoped step, or the per-stage one (F1) whose U1
+    // "refill" is then a barrier: every rank's stage 1 (its U1 and the U1
+    // x-guards it wrote into other ranks' blocks) before any stage 2 reads them
+    if (only >= 0 || !(xonly || xonly_u1))
+      return fail(ORCHA_E_STATE, "peer mode needs the gather fills (fill mode 1, fused kernels, one packet, no "
+                                 "guard push)");
+    if (buffer == 1 || !(pk[0]->xguards_pushed && pk[0]->push_plan == f)) {
+      // buffer 0 after a pack: the x-guard fill reads other ranks' interiors,
+      // so every rank's pack must be done
+      rc = comm_peer_barrier(f->peer, s);
+      if (rc) return rc;
+    }
+  }
   if (xonly_u1) {
     if (f->edge_fix[0]) {  // exchanged rows' resident-sourced x-guard parts
       cudaError_t e = launch_fill(G0, pk[0]->scratch, pk[0]->nslots, f->d_tables_u1[0], s, 2);

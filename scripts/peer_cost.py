@@ -128,10 +128,35 @@ def measure(grid, steps=10, warmup=3):
         c.check()
         c.destroy()
     del pks
+    # F1 + F2: the per-stage step in peer mode (U1 rows read from the other
+    # ranks' stage-1 buffers; the U1 refill is a barrier)
+    g, comms, pks = setup(grid)
+    for r in range(R):
+        comms[r].peer_register(pks[r])
+    for r in range(R):
+        hydro.orcha_fill_prepare([pks[r]], comms[r])
+    clocks = [hydro.DevClock() for _ in range(R)]
+
+    def step_ps():
+        for r in range(R):
+            hydro.orcha_fill_guardcells_stage([pks[r]], 0, comms[r], streams[r])
+        for r in range(R):
+            hydro.orcha_compute_dt_device([pks[r]], clocks[r], comms[r], streams[r])
+        for r in range(R):
+            hydro.orcha_hydro_stage_devdt(pks[r], 1, clocks[r].dt_tensor, streams[r])
+        for r in range(R):
+            hydro.orcha_fill_guardcells_stage([pks[r]], 1, comms[r], streams[r])
+        for r in range(R):
+            hydro.orcha_hydro_stage_devdt(pks[r], 2, clocks[r].dt_tensor, streams[r])
+    out["peer_per_stage_ms_per_rank_step"] = timed(step_ps, streams, steps, warmup) / R
+    for c in comms:
+        c.check()
+        c.destroy()
+    del pks
     return out
 
 
-def single(steps=10, warmup=3):
+def single(steps=10, warmup=3, method="telescoped"):
     g, comms, pks = setup((1, 1, 1))
     for c in comms:
         c.destroy()
@@ -139,9 +164,12 @@ def single(steps=10, warmup=3):
     clock = hydro.DevClock()
 
     def step():
-        hydro.orcha_fill_guardcells(pks, None, s)
+        if method == "per-stage":
+            hydro.orcha_fill_guardcells_stage(pks, 0, None, s)
+        else:
+            hydro.orcha_fill_guardcells(pks, None, s)
         hydro.orcha_compute_dt_device(pks, clock, None, s)
-        hydro.orcha_hydro_advance_devdt(pks[0], clock.dt_tensor, s)
+        hydro.step_devdt(pks, clock.dt_tensor, None, s, method)
     return timed(step, [s], steps, warmup)
 
 
@@ -150,12 +178,14 @@ def main():
     lib = abi.load(False)
     abi.call(lib, "orcha_set_fill_mode", 1)
     one = single()
+    one_ps = single(method="per-stage")
     rows = [measure(gr) for gr in ((2, 1, 1), (2, 2, 1), (2, 2, 2))]
     for r in rows:
+        r["peer_per_stage_vs_single_telescoped"] = r["peer_per_stage_ms_per_rank_step"] / one - 1.0
         r["exchange_overhead_vs_single"] = r["exchange_ms_per_rank_step"] / one - 1.0
         r["peer_overhead_vs_single"] = r["peer_ms_per_rank_step"] / one - 1.0
         r["overlap_overhead_vs_single"] = r["overlap_ms_per_rank_step"] / one - 1.0
-    print(json.dumps({"single_rank_ms_per_step": one, "rows": rows, "gpu": torch.cuda.get_device_name(0),
+    print(json.dumps({"single_rank_ms_per_step": one, "single_rank_per_stage_ms_per_step": one_ps, "rows": rows, "gpu": torch.cuda.get_device_name(0),
                       "note": "virtual ranks on one GPU, each with cfg4's 4096-block brick; per-rank step = "
                               "the R-rank step / R; no NVLink wire time is included in either path"}))
 

@@ -2,7 +2,7 @@
 PROCESSES (CUDA IPC), launched by torch.distributed.run with every rank on
 GPU 0; gloo carries only the IPC blobs and the results.
 
-  python -m torch.distributed.run --nproc-per-node R tests/ipc_worker.py OUT parity|production STEPS CASE
+  python -m torch.distributed.run --nproc-per-node R tests/ipc_worker.py OUT parity|production STEPS CASE [METHOD]
 """
 import os
 import pickle
@@ -27,6 +27,7 @@ CASES = {
 
 def main():
     out, mode, steps, case = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
+    method = sys.argv[5] if len(sys.argv) > 5 else "telescoped"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
     dist.init_process_group("gloo")
@@ -48,9 +49,16 @@ def main():
     s = torch.cuda.current_stream()
     log = []
     for _ in range(steps):
-        hydro.orcha_fill_guardcells([pk], comm, s)
-        hydro.orcha_compute_dt_device([pk], clock, comm, s)
-        hydro.orcha_hydro_advance_devdt(pk, clock.dt_tensor, s)
+        if method == "per-stage":
+            hydro.orcha_fill_guardcells_stage([pk], 0, comm, s)
+            hydro.orcha_compute_dt_device([pk], clock, comm, s)
+            hydro.orcha_hydro_stage_devdt(pk, 1, clock.dt_tensor, s)
+            hydro.orcha_fill_guardcells_stage([pk], 1, comm, s)
+            hydro.orcha_hydro_stage_devdt(pk, 2, clock.dt_tensor, s)
+        else:
+            hydro.orcha_fill_guardcells([pk], comm, s)
+            hydro.orcha_compute_dt_device([pk], clock, comm, s)
+            hydro.orcha_hydro_advance_devdt(pk, clock.dt_tensor, s)
         s.synchronize()
         c = clock.read()
         log.append((c.dt, c.smax, c.argmax, c.tag))

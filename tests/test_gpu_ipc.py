@@ -38,13 +38,13 @@ def _port():
     return p
 
 
-def _run_ranks(tmp_path, case, mode, steps):
+def _run_ranks(tmp_path, case, mode, steps, method="telescoped"):
     nranks = int(np.prod(ipc_worker.CASES[case][3]))
-    out = str(tmp_path / f"ipc_{case}_{mode}.pkl")
+    out = str(tmp_path / f"ipc_{case}_{mode}_{method}.pkl")
     env = dict(os.environ, ORCHA_PEER_TIMEOUT_MS="60000", PYTHONPATH=ROOT)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "ipc_worker.py"), out, mode, str(steps), case]
+           os.path.join(ROOT, "tests", "ipc_worker.py"), out, mode, str(steps), case, method]
     r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-4000:]
     return pickle.load(open(out, "rb"))
@@ -64,6 +64,18 @@ def test_ipc_peer_mode_bitwise_equal_single_domain(tmp_path, case):
     U0 = inp.sedov(g.N) if ic == "sedov" else inp.random_field(g.N, seed=91)
     A, _, logA, _ = H.gpu_run(g, U0, nsteps=4)
     allr = _run_ranks(tmp_path, case, "production", 4)
+    for _, _, log in allr:
+        assert log == [tuple(x) for x in logA]
+    assert np.array_equal(_assemble(g, allr), A)
+
+
+def test_ipc_peer_mode_per_stage_variant(tmp_path):
+    # F1 + F2 across processes: U1 rows read from other processes' stage-1 buffers
+    nb, nblk, bc, gg, brick, ic = ipc_worker.CASES["random16"]
+    g = H.make_grid(3, nb, nblk, bc=bc)
+    U0 = inp.random_field(g.N, seed=91)
+    A, _, logA, _ = H.gpu_run(g, U0, nsteps=3, method="per-stage")
+    allr = _run_ranks(tmp_path, "random16", "production", 3, method="per-stage")
     for _, _, log in allr:
         assert log == [tuple(x) for x in logA]
     assert np.array_equal(_assemble(g, allr), A)

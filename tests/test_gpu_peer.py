@@ -46,7 +46,7 @@ def _setup(g, U0, owner):
     return comms, streams, pks
 
 
-def _run_peer(g, U0, owner, nsteps):
+def _run_peer(g, U0, owner, nsteps, method="telescoped"):
     """Device-dt loop, ranks interleaved on their own streams."""
     import torch
     from paper_2507_09337_b200 import hydro
@@ -57,12 +57,25 @@ def _run_peer(g, U0, owner, nsteps):
     launches = []
     for _ in range(nsteps):
         c0 = g.lib.orcha_launch_count()
-        for r in range(n):
-            hydro.orcha_fill_guardcells([pks[r]], comms[r], streams[r])
-        for r in range(n):
-            hydro.orcha_compute_dt_device([pks[r]], clocks[r], comms[r], streams[r])
-        for r in range(n):
-            hydro.orcha_hydro_advance_devdt(pks[r], clocks[r].dt_tensor, streams[r])
+        if method == "per-stage":
+            # F1 in peer mode: the U1 "refill" is the barrier between the stages
+            for r in range(n):
+                hydro.orcha_fill_guardcells_stage([pks[r]], 0, comms[r], streams[r])
+            for r in range(n):
+                hydro.orcha_compute_dt_device([pks[r]], clocks[r], comms[r], streams[r])
+            for r in range(n):
+                hydro.orcha_hydro_stage_devdt(pks[r], 1, clocks[r].dt_tensor, streams[r])
+            for r in range(n):
+                hydro.orcha_fill_guardcells_stage([pks[r]], 1, comms[r], streams[r])
+            for r in range(n):
+                hydro.orcha_hydro_stage_devdt(pks[r], 2, clocks[r].dt_tensor, streams[r])
+        else:
+            for r in range(n):
+                hydro.orcha_fill_guardcells([pks[r]], comms[r], streams[r])
+            for r in range(n):
+                hydro.orcha_compute_dt_device([pks[r]], clocks[r], comms[r], streams[r])
+            for r in range(n):
+                hydro.orcha_hydro_advance_devdt(pks[r], clocks[r].dt_tensor, streams[r])
         torch.cuda.synchronize()
         launches.append(g.lib.orcha_launch_count() - c0)
         recs = [(c.dt, c.smax, c.argmax, c.tag) for c in (k.read() for k in clocks)]
@@ -113,6 +126,26 @@ def test_peer_mode_with_scheme_variants(scheme):
     B, logB, _ = _run_peer(g, U0, owner, 4)
     assert logB == [tuple(x) for x in logA]
     assert np.array_equal(A, B)
+
+
+@pytest.mark.parametrize("case", [CASES[1], CASES[2]])
+def test_peer_mode_per_stage_variant(case):
+    # F1 + F2: the per-stage step in peer mode (U1 rows staged from other
+    # ranks' stage-1 buffers, a barrier as the U1 refill) == the single-domain
+    # per-stage step; parity build == the oracle's refill mode
+    from paper_2507_09337_b200 import hydro
+    ndim, nb, nblk, bc, gg, brick = case
+    for parity in (False, True):
+        g = H.make_grid(ndim, nb, nblk, bc=bc, parity=parity)
+        owner = hydro.brick_owner(nblk, brick, gg)
+        U0 = inp.random_field(g.N, seed=74)
+        A, _, logA, _ = H.gpu_run(g, U0, nsteps=4, method="per-stage")
+        B, logB, launches = _run_peer(g, U0, owner, 4, method="per-stage")
+        assert logB == [tuple(x) for x in logA]
+        assert np.array_equal(A, B)
+        if parity:
+            Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4, mode="refill")
+            assert np.array_equal(B, Oo)
 
 
 def test_peer_mode_scattered_owner_map():

@@ -755,8 +755,13 @@ static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int ns
     s2 = s2v;
     if (parts & 1) {
       PhaseScope ph(PH_STAGE1, s);
+#ifdef ORCHA_SPLIT1_ONE  // experiment: one CTA per block for stage 1 (20 rows, 22 warps, 1 CTA per SM)
+      (void)s1;
+      launch_stage<NB, 1, 1, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+#else
       if (s1 == 4) launch_stage<NB, 1, 4, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
       else launch_stage<NB, 1, 2, 0, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, nullptr, nbr);
+#endif
     }
     if (parts & 2) {
       PhaseScope ph(PH_STAGE2, s);

@@ -770,7 +770,9 @@ def main():
                            same_gpu=(True if same_gpu else None)),
             "roofline": primary, "roofline_other": other, "roofline_issue": roof_issue,
             "hbm_fraction_full_step": {"achieved_gbs": step_hbm, "frac": step_hbm / pks["hbm_gbs"],
-                                       "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes},
+                                       "frac_of_nominal_8tbs": step_hbm / 8000.0,
+                                       "algorithmic_bytes_per_cell_update": adv_bytes + fill_bytes,
+                                       "dram_bytes_per_cell_update_ncu": (traffic / cu_local) if traffic else None},
             "advance_ms": adv_ms, "method": args.method, "dt_mode": args.dt_mode, "variants": variants,
             "clocks": clk, "gpu_launches": int(launches), "e2e": e2e, "e2e_serial": e2e_serial,
             "floor_hits": fh, "nonphysical_first_cell": bad,

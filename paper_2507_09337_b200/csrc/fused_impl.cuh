@@ -87,7 +87,8 @@
 #ifndef ORCHA_ONEBAR
 #define ORCHA_ONEBAR 0
 #endif
-// z-face carry (ORCHA_ZCARRY, per stage: bit 0 stage 1, bit 1 stage 2): the
+// z-face carry (ORCHA_ZCARRY: bit 0 stage 1, bit 1 telescoped stage 2, bit 2
+// per-stage stage 2; only bit 0 measured faster -- profiles/r02_ab_zcarry*.txt): the
 // z-face task of a column computes the z-slope of cell k+1 once and keeps
 // its upper face state q + s/2 (the left state of face k+3/2) in a
 // per-column shared slot for the next plane, instead of recomputing that
@@ -188,7 +189,9 @@ struct Geo {
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
   // z-face carry slots; not for 8^3 blocks, whose stage 1 fits 3 CTAs per SM
   // without them and 2 with (measured: 3.09 -> 2.59 G cu/s for one packet)
-  static constexpr bool ZC = ((ORCHA_ZCARRY >> (STAGE - 1)) & 1) && NB >= 16;
+  // (bit 0: stage 1 of both methods; bit 1: the telescoped stage 2; bit 2:
+  // the per-stage variant's stage 2)
+  static constexpr bool ZC = ((ORCHA_ZCARRY >> (STAGE == 1 ? 0 : MODE == 1 ? 2 : 1)) & 1) && NB >= 16;
   static constexpr size_t SMEM =
       sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ + (ZC ? 5 * FZ : 0)) + 64 +
       ((NS * IR + 15) / 16) * 16;

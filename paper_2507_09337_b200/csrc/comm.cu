@@ -911,6 +911,11 @@ extern "C" int32_t orcha_comm_ipc_attach(orcha_comm* c, const void* blobs, size_
   if (!c || !blobs) return fail(ORCHA_E_ARG, "null argument");
   if (!c->ipc || !c->own_packet) return fail(ORCHA_E_STATE, "orcha_comm_ipc_export first");
   if (c->peer_mode) return fail(ORCHA_E_STATE, "already attached");
+  // a failed earlier attempt: release what it mapped before trying again
+  for (void* p : c->ipc_mapped) cudaIpcCloseMemHandle(p);
+  c->ipc_mapped.clear();
+  for (auto* p : c->shadow) delete p;
+  c->shadow.clear();
   std::vector<unsigned long long*> ctr(c->nranks, nullptr);
   c->peer_gather.assign(c->nranks, nullptr);
   for (int q = 0; q < c->nranks; q++) {

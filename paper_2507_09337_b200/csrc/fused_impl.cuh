@@ -243,24 +243,48 @@ __device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, i
   }
 }
 
+// Borrowed-ring telescoped step (HYB = 1, stage 1): interior cell (ci, cj, k)
+// of U1 also writes the x-ring (2 deep) of the compact U1 cube of the
+// x-neighbour the hybrid push table names (nullptr: that neighbour computes
+// its ring itself).  sxp[0] = the -x neighbour (fed by ci < 2), sxp[1] = +x.
+template <int NB>
+__device__ __forceinline__ void push_x_u1(const PushEntry* sxp, long long U1C, int ci, int cj, int k,
+                                          const double w[5]) {
+  if (ci < 0 || ci >= NB || cj < 0 || cj >= NB || k < 0 || k >= NB) return;
+  const int side = ci < 2 ? 0 : (ci >= NB - 2 ? 1 : -1);
+  if (side < 0) return;
+  double* d = sxp[side].dst;
+  if (d == nullptr) return;
+  const int t = side ? ci - NB : ci + NB;
+  double* q = d + ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (t + 2);
+#pragma unroll
+  for (int v = 0; v < 5; v++) q[v * U1C] = w[v];
+}
+
 // PUSH: 0 none, 1 scatter the new state into every same-packet guard
 // (push_cell), 2 into the x-guards only (push_x, gather mode).
 // GATHER: the gather-mode staging (nbr is the per-slot neighbour table); a
 // separate instantiation so the plain kernels carry none of its registers.
 // SCH: 0 the paper-path scheme, 1 the grid's F4 flags (see face_flux).
-template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER, int SCH>
+// HYB: 1 = a stage-1 kernel of the borrowed-ring telescoped step (see
+// launch_hybrid_nb): U1 always in the compact (n+4)^3 cubes, the CTA's slot
+// and its self-ring sides from smap (slot | mask << 26), ring cells written
+// only on self sides, the x-ring of the x-neighbours pushed (push_x_u1).
+template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER, int SCH, int HYB = 0>
 __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
                        DtRecord* __restrict__ rec, DevStatus* st, const PushEntry* __restrict__ push,
-                       const NbrEntry* __restrict__ nbr) {
+                       const NbrEntry* __restrict__ nbr, const int* __restrict__ smap) {
   using Gm = Geo<NB, STAGE, SPLIT, MODE>;
   constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
   constexpr int NT = Gm::NT, H = Gm::H, ORG = Gm::ORG;
-  // U1 cube stride: (n+4)^3 compact scratch (telescoped) or the padded state layout (per-stage)
-  const long long U1C = (MODE == 0) ? u1_cube<NB>() : G.cube;
+  // U1 cube stride: (n+4)^3 compact scratch (telescoped, and every hybrid
+  // kernel) or the padded state layout (per-stage)
+  constexpr bool CU1 = MODE == 0 || HYB;
+  const long long U1C = CU1 ? u1_cube<NB>() : G.cube;
   auto u1_off = [&](int ci, int cj, int k) -> long long {
-    return (MODE == 0) ? ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2) : cell_off(G, ci, cj, k);
+    return CU1 ? ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2) : cell_off(G, ci, cj, k);
   };
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;                                   // [NS][5][IR][IPX]
@@ -272,7 +296,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   unsigned char* flipm = reinterpret_cast<unsigned char*>(bar + 8);  // [NS][IR]
 
   const int tid = threadIdx.x;
-  const long long slot = blockIdx.x / Gm::NSPLIT;
+  const int me = HYB ? smap[blockIdx.x / Gm::NSPLIT] : (int)(blockIdx.x / Gm::NSPLIT);
+  const long long slot = HYB ? (me & 0x3ffffff) : me;
+  const int selfm = HYB ? (me >> 26) : 0;  // self-ring sides: bit 2a (-a), 2a+1 (+a)
   const int band = blockIdx.x % Gm::NSPLIT;
   const int jj0 = band * H;                              // first output row of the band (0-based)
   const long long cube = G.cube;
@@ -282,7 +308,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const SlotInfo si = slots[slot];
 
   __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
-  if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
+  if ((PUSH == 2 || (HYB && STAGE == 1)) && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
   __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
   if (GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
   constexpr int UWARPS = (Gm::FZ + 31) / 32;  // warps with update cells
@@ -626,7 +652,25 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         if (lane == 0) mbar_arrive(fdone);
       }
       if (upd) {
-      if (STAGE == 1) {
+      if (STAGE == 1 && HYB) {
+        // borrowed-ring step: a box ring cell is written only on a self side
+        // (the other sides' rings are the neighbours' own cells: their x-ring
+        // is pushed by them, their y/z rows are staged from them by stage 2);
+        // edge and corner cells of the box are read by no stage-2 stencil
+        const int ax = ci < 0 ? 0 : ci >= NB ? 1 : -1, ay = cj < 0 ? 2 : cj >= NB ? 3 : -1,
+                  az = k < 0 ? 4 : k >= NB ? 5 : -1;
+        const int nout = (ax >= 0) + (ay >= 0) + (az >= 0);
+        const int sb = ax >= 0 ? ax : ay >= 0 ? ay : az;
+        double w[5];
+#pragma unroll
+        for (int v = 0; v < 5; v++) w[v] = un[v] - dt * D[v];
+        if (nout == 0 || (nout == 1 && ((selfm >> sb) & 1))) {
+          double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
+#pragma unroll
+          for (int v = 0; v < 5; v++) out[v * U1C] = w[v];
+        }
+        push_x_u1<NB>(sxp, U1C, ci, cj, k, w);
+      } else if (STAGE == 1) {
         double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
 #pragma unroll
         for (int v = 0; v < 5; v++) out[v * U1C] = un[v] - dt * D[v];
@@ -715,7 +759,7 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
 #define ORCHA_K(P, GT)                                                                                  \
   stage_fused_kernel<NB, STAGE, SPLIT, MODE, P, GT, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, \
                                                                                       d_dt, h_dt, records, st, \
-                                                                                      push, nbr)
+                                                                                      push, nbr, nullptr)
   if (push && pushkind == 2) {
     if constexpr (P2) {
       if constexpr (GA) {
@@ -813,6 +857,73 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
   return cudaGetLastError();
 }
 
+// ------------------------------------------- borrowed-ring telescoped step --
+// The paper's telescoping computes stage 1 on the block plus a 2-cell ring so
+// that stage 2 needs no second guard exchange (sec 6).  A ring
+// cell whose owner block is resident in the same packet is that owner's own
+// stage-1 value: the owner computes it from the same U^n cells (the guards
+// are copies of them), so the telescoped result is unchanged when the ring is
+// borrowed from the owner instead of recomputed.  Only "self" sides -- a
+// physical boundary (the ring is U1 of the BC-imaged U^n, which no block
+// owns) or an owner on another rank (no second exchange) -- need the ring
+// computed.  So stage 1 runs in two launches over the slot map:
+//   smap[0, nbnd):        blocks with a self side, the box kernel (MODE 0
+//                         geometry), ring cells stored on self sides only;
+//   smap[nbnd, +nint):    the rest, interior only (MODE 1 geometry);
+// both write U1 into the compact (n+4)^3 cubes and push their x-boundary
+// columns into the x-ring of the x-neighbours (hpush); stage 2 is the
+// telescoped stage-2 kernel staging its y/z ring rows from the owners' cubes
+// (hnbr; nullptr = its own cube: self side).  Stage-1 work per block: 1x
+// instead of (n+4)^3/n^3 (1.95x at 16^3, 3.4x at 8^3) away from self sides.
+template <int NB, int SCH>
+static cudaError_t hybrid_attrs() {
+  constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
+  static cudaError_t once = [] {
+    cudaError_t e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 0>::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 2, true, SCH, 0>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 2, S, 0>::SMEM);
+    return e;
+  }();
+  return once;
+}
+
+template <int NB, int SCH>
+static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
+                                    const int* smap, int nbnd, int nint, const PushEntry* hpush,
+                                    const NbrEntry* nbr, const NbrEntry* hnbr, const double* d_dt, double h_dt,
+                                    DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s,
+                                    const PushEntry* push, int parts) {
+  constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
+  cudaError_t e = hybrid_attrs<NB, SCH>();
+  if (e != cudaSuccess) return e;
+  if (parts & 1) {
+    PhaseScope ph(PH_STAGE1, s);
+    if (nbnd > 0) {
+      stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1><<<nbnd * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM, s>>>(
+          G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap);
+      count_launch();
+    }
+    if (nint > 0) {
+      stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM, s>>>(
+          G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap + nbnd);
+      count_launch();
+    }
+  }
+  if (parts & 2) {
+    PhaseScope ph(PH_STAGE2, s);
+    stage_fused_kernel<NB, 2, S, 0, 2, true, SCH, 0><<<nslots * S, Geo<NB, 2, S, 0>::NT, Geo<NB, 2, S, 0>::SMEM, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, push, hnbr, nullptr);
+    count_launch();
+    *nrecords = (long long)nslots * S;
+  }
+  return cudaGetLastError();
+}
+
 // Load (CUDA lazy loading) the telescoped gather-mode kernels of this block
 // size and scheme ahead of time, with their shared-memory attribute: loading
 // mid-step may wait for an idle device (F2 peer mode: a rank spinning in a
@@ -842,6 +953,18 @@ static cudaError_t preload_nb() {
     return launch_stage_nb<NB, SCH>(G, stage, state, u1, nslots, slots, d_dt, h_dt, records, nrecords, st, s,   \
                                     push, nbr, pk);                                                              \
   }                                                                                                              \
-  cudaError_t fused_preload_n##NB##_s##SCH() { return preload_nb<NB, SCH>(); }
+  cudaError_t fused_preload_n##NB##_s##SCH() {                                                                   \
+    cudaError_t e = preload_nb<NB, SCH>();                                                                       \
+    return e == cudaSuccess ? hybrid_attrs<NB, SCH>() : e;                                                       \
+  }                                                                                                              \
+  cudaError_t fused_hybrid_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,              \
+                                          const SlotInfo* slots, const int* smap, int nbnd, int nint,            \
+                                          const PushEntry* hpush, const NbrEntry* nbr, const NbrEntry* hnbr,     \
+                                          const double* d_dt, double h_dt, DtRecord* records,                    \
+                                          long long* nrecords, DevStatus* st, cudaStream_t s,                    \
+                                          const PushEntry* push, int parts) {                                    \
+    return launch_hybrid_nb<NB, SCH>(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, hnbr, d_dt, h_dt, \
+                                     records, nrecords, st, s, push, parts);                                      \
+  }
 
 }  // namespace orcha

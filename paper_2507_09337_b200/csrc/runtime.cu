@@ -68,6 +68,11 @@ cudaError_t launch_stage_fused(const DevGrid& G, int stage, double* state, doubl
 bool fused_supported(const DevGrid& G);
 cudaError_t fused_preload(const DevGrid& G);
 long long fused_u1_cube(int nb);
+cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
+                                  const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
+                                  const NbrEntry* hnbr, const double* d_dt, double h_dt, DtRecord* records,
+                                  long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
+                                  int parts);
 }  // namespace orcha
 
 // Fill mode: 1 = gather (default): when every guard source of the packet set
@@ -103,6 +108,24 @@ extern "C" int32_t orcha_set_guard_push(int32_t on) {
   g_push = on ? 1 : 0;
   return ORCHA_OK;
 }
+
+// Ring mode of the telescoped step (orcha_set_ring_mode): 1 = borrowed ring
+// (default; fused_impl.cuh launch_hybrid_nb), 0 = every block computes its
+// whole stage-1 ring.  Env ORCHA_RING overrides the default.
+static int g_ring = -1;
+static int ring_mode() {
+  if (g_ring < 0) {
+    const char* e = getenv("ORCHA_RING");
+    g_ring = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return g_ring;
+}
+extern "C" int32_t orcha_set_ring_mode(int32_t mode) {
+  if (mode != 0 && mode != 1) return fail(ORCHA_E_ARG, "ring mode must be 0 (computed) or 1 (borrowed)");
+  g_ring = mode;
+  return ORCHA_OK;
+}
+extern "C" int32_t orcha_get_ring_mode(void) { return ring_mode(); }
 
 extern "C" const char* orcha_last_error(void) { return g_last_error.c_str(); }
 extern "C" int64_t orcha_launch_count(void) { return g_launches.load(); }
@@ -224,6 +247,13 @@ struct FillPlan {
   SlotFill* d_sf = nullptr;
   SlotFill* d_sf_u1 = nullptr;
   long long nslots_total = 0;
+  // borrowed-ring telescoped step (one packet, not peer mode; fused_impl.cuh
+  // launch_hybrid_nb): the slot map (slots with a self side first, each entry
+  // slot | self-side mask << 26), the x-ring push table and the U1 row table
+  int* d_hyb_smap = nullptr;
+  int hyb_nbnd = 0, hyb_nint = 0;
+  PushEntry* d_hyb_push = nullptr;
+  NbrEntry* d_hyb_nbr = nullptr;
 };
 // Frees a plan's device tables and the plan (not its packets' pointers).
 static void free_plan_tables(FillPlan* f) {
@@ -235,6 +265,9 @@ static void free_plan_tables(FillPlan* f) {
   for (auto* t : f->d_cross_u1) cudaFree(t);
   cudaFree(f->d_sf);
   cudaFree(f->d_sf_u1);
+  cudaFree(f->d_hyb_smap);
+  cudaFree(f->d_hyb_push);
+  cudaFree(f->d_hyb_nbr);
   delete f;
 }
 
@@ -725,6 +758,67 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     f->d_cross.push_back(dx);
     f->d_cross_u1.push_back(dx1);
   }
+  if (npk == 1 && !peer && fused_supported(G)) {
+    // borrowed-ring telescoped step: a side of a block is "self" when its
+    // neighbour is not a resident block of this packet reached by a shift
+    // (physical boundary: clamp / mirror; another rank or packet) -- there
+    // the block computes its stage-1 ring itself, elsewhere it borrows it
+    orcha_packet* p = pk[0];
+    const long long U1C = fused_u1_cube(G.nb[0]);
+    std::vector<int> bnd, inr;
+    std::vector<PushEntry> hp((size_t)p->nslots * 27, PushEntry{nullptr, 0, 0});
+    std::vector<NbrEntry> hn((size_t)p->nslots * 27, NbrEntry{nullptr, 0, 0});
+    auto local_slot = [&](const int bc[3], const int o[3], int* mode) -> int {
+      HostEntry h = make_entry(g, bc, o);
+      *mode = h.mode;
+      for (int a = 0; a < 3; a++)
+        if (o[a] != 0 && ((h.mode >> (2 * a)) & 3) != kShift) return -1;
+      auto it = where.find(h.src_block);
+      return (it == where.end() || it->second.first != 0) ? -1 : it->second.second;
+    };
+    for (int s = 0; s < p->nslots; s++) {
+      long long b = p->ids[s];
+      int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
+                   (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+      int mask = 0, md = 0;
+      for (int a = 0; a < 3; a++)
+        for (int sd = 0; sd < 2; sd++) {
+          int o[3] = {0, 0, 0};
+          o[a] = sd ? 1 : -1;
+          const int ns = local_slot(bc, o, &md);
+          if (ns < 0) mask |= 1 << (2 * a + sd);
+          else if (a == 0) hp[(size_t)s * 27 + (sd ? 14 : 12)] = PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
+        }
+      for (int oz = -1; oz <= 1; oz++)
+        for (int oy = -1; oy <= 1; oy++) {
+          if (oy == 0 && oz == 0) continue;
+          const bool self = (oy != 0 && ((mask >> (2 + (oy > 0))) & 1)) || (oz != 0 && ((mask >> (4 + (oz > 0))) & 1));
+          int o[3] = {0, oy, oz};
+          const int ns = self ? -1 : local_slot(bc, o, &md);
+          if (ns >= 0)
+            hn[(size_t)s * 27 + (oz + 1) * 9 + (oy + 1) * 3 + 1] =
+                NbrEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
+        }
+      (mask ? bnd : inr).push_back(s | (mask << 26));
+    }
+    std::vector<int> smap = bnd;
+    smap.insert(smap.end(), inr.begin(), inr.end());
+    f->hyb_nbnd = (int)bnd.size();
+    f->hyb_nint = (int)inr.size();
+    cudaError_t err = cudaMalloc(&f->d_hyb_smap, smap.size() * sizeof(int));
+    if (err == cudaSuccess)
+      err = cudaMemcpy(f->d_hyb_smap, smap.data(), smap.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&f->d_hyb_push, hp.size() * sizeof(PushEntry));
+    if (err == cudaSuccess)
+      err = cudaMemcpy(f->d_hyb_push, hp.data(), hp.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMalloc(&f->d_hyb_nbr, hn.size() * sizeof(NbrEntry));
+    if (err == cudaSuccess)
+      err = cudaMemcpy(f->d_hyb_nbr, hn.data(), hn.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) {
+      free_plan_tables(f);
+      return cuda_fail(err, "upload borrowed-ring tables");
+    }
+  }
   if (npk > 1) {
     std::vector<SlotFill> sf, sf1;
     for (int q = 0; q < npk; q++)
@@ -1104,6 +1198,11 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   if (!fused)
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
+  else if (!p->peer_comm && xpush && ring_mode() == 1 && p->push_plan->d_hyb_smap &&
+           p->d_nbr == p->push_plan->d_tables[0])
+    e = launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, p->push_plan->d_hyb_smap,
+                              p->push_plan->hyb_nbnd, p->push_plan->hyb_nint, p->push_plan->d_hyb_push, p->d_nbr,
+                              p->push_plan->d_hyb_nbr, d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3);
   else if (!p->peer_comm)
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                              &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr, xpush);

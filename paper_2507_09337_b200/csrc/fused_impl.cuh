@@ -244,21 +244,29 @@ __device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, i
 }
 
 // Borrowed-ring telescoped step (HYB = 1, stage 1): interior cell (ci, cj, k)
-// of U1 also writes the x-ring (2 deep) of the compact U1 cube of the
-// x-neighbour the hybrid push table names (nullptr: that neighbour computes
-// its ring itself).  sxp[0] = the -x neighbour (fed by ci < 2), sxp[1] = +x.
+// of U1 also writes the ring (2 deep) of the compact U1 cubes of the face
+// neighbours the hybrid push table names (nullptr: that neighbour computes
+// its ring itself).  sxp[2a] = the -a neighbour (fed by cells with coordinate
+// a < 2), sxp[2a+1] = the +a neighbour (coordinate >= n-2); a cell near an
+// edge feeds each face neighbour separately (edge cells of the ring are read
+// by no stage-2 stencil).
 template <int NB>
-__device__ __forceinline__ void push_x_u1(const PushEntry* sxp, long long U1C, int ci, int cj, int k,
-                                          const double w[5]) {
+__device__ __forceinline__ void push_u1(const PushEntry* sxp, long long U1C, int ci, int cj, int k,
+                                        const double w[5]) {
   if (ci < 0 || ci >= NB || cj < 0 || cj >= NB || k < 0 || k >= NB) return;
-  const int side = ci < 2 ? 0 : (ci >= NB - 2 ? 1 : -1);
-  if (side < 0) return;
-  double* d = sxp[side].dst;
-  if (d == nullptr) return;
-  const int t = side ? ci - NB : ci + NB;
-  double* q = d + ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (t + 2);
+  const int c[3] = {ci, cj, k};
 #pragma unroll
-  for (int v = 0; v < 5; v++) q[v * U1C] = w[v];
+  for (int a = 0; a < 3; a++) {
+    const int side = c[a] < 2 ? 0 : (c[a] >= NB - 2 ? 1 : -1);
+    if (side < 0) continue;
+    double* d = sxp[2 * a + side].dst;
+    if (d == nullptr) continue;
+    int t[3] = {ci, cj, k};
+    t[a] = side ? c[a] - NB : c[a] + NB;
+    double* q = d + ((long long)(t[2] + 2) * (NB + 4) + (t[1] + 2)) * (NB + 4) + (t[0] + 2);
+#pragma unroll
+    for (int v = 0; v < 5; v++) q[v * U1C] = w[v];
+  }
 }
 
 // PUSH: 0 none, 1 scatter the new state into every same-packet guard
@@ -298,7 +306,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const int tid = threadIdx.x;
   const int me = HYB ? smap[blockIdx.x / Gm::NSPLIT] : (int)(blockIdx.x / Gm::NSPLIT);
   const long long slot = HYB ? (me & 0x3ffffff) : me;
-  const int selfm = HYB ? (me >> 26) : 0;  // self-ring sides: bit 2a (-a), 2a+1 (+a)
+  const int selfm = HYB ? ((me >> 26) & 63) : 0;  // self-ring sides: bit 2a (-a), 2a+1 (+a)
   const int band = blockIdx.x % Gm::NSPLIT;
   const int jj0 = band * H;                              // first output row of the band (0-based)
   const long long cube = G.cube;
@@ -307,8 +315,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const long long in_cube = (STAGE == 1) ? cube : U1C;
   const SlotInfo si = slots[slot];
 
-  __shared__ PushEntry sxp[2];  // PUSH == 2: the -x / +x push targets of this block
-  if ((PUSH == 2 || (HYB && STAGE == 1)) && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
+  // PUSH == 2: the -x / +x push targets of this block; HYB stage 1: the six
+  // face neighbours' (-x, +x, -y, +y, -z, +z)
+  __shared__ PushEntry sxp[6];
+  if (PUSH == 2 && tid < 2) sxp[tid] = push[slot * 27 + (tid ? 14 : 12)];
+  if (HYB && STAGE == 1 && tid < 6) sxp[tid] = push[slot * 27 + (tid == 0 ? 12 : tid == 1 ? 14 : tid == 2 ? 10 : tid == 3 ? 16 : tid == 4 ? 4 : 22)];
   __shared__ NbrEntry snb[9];   // gather mode: the (0, oy, oz) neighbour entries of this block
   if (GATHER && tid < 9) snb[tid] = nbr[slot * 27 + (tid / 3) * 9 + (tid % 3) * 3 + 1];
   constexpr int UWARPS = (Gm::FZ + 31) / 32;  // warps with update cells
@@ -669,7 +680,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 #pragma unroll
           for (int v = 0; v < 5; v++) out[v * U1C] = w[v];
         }
-        push_x_u1<NB>(sxp, U1C, ci, cj, k, w);
+        push_u1<NB>(sxp, U1C, ci, cj, k, w);
       } else if (STAGE == 1) {
         double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
 #pragma unroll
@@ -870,10 +881,9 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
 //   smap[0, nbnd):        blocks with a self side, the box kernel (MODE 0
 //                         geometry), ring cells stored on self sides only;
 //   smap[nbnd, +nint):    the rest, interior only (MODE 1 geometry);
-// both write U1 into the compact (n+4)^3 cubes and push their x-boundary
-// columns into the x-ring of the x-neighbours (hpush); stage 2 is the
-// telescoped stage-2 kernel staging its y/z ring rows from the owners' cubes
-// (hnbr; nullptr = its own cube: self side).  Stage-1 work per block: 1x
+// both write U1 into the compact (n+4)^3 cubes and push their 2-cell
+// boundary layers into the ring of the face neighbours' cubes (hpush), so
+// stage 2 is the plain telescoped stage-2 kernel over complete cubes.  Stage-1 work per block: 1x
 // instead of (n+4)^3/n^3 (1.95x at 16^3, 3.4x at 8^3) away from self sides.
 template <int NB, int SCH>
 static cudaError_t hybrid_attrs() {
@@ -885,7 +895,7 @@ static cudaError_t hybrid_attrs() {
       e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 2, true, SCH, 0>,
+      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 2, S, 0>::SMEM);
     return e;
   }();
@@ -895,7 +905,7 @@ static cudaError_t hybrid_attrs() {
 template <int NB, int SCH>
 static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                     const int* smap, int nbnd, int nint, const PushEntry* hpush,
-                                    const NbrEntry* nbr, const NbrEntry* hnbr, const double* d_dt, double h_dt,
+                                    const NbrEntry* nbr, const double* d_dt, double h_dt,
                                     DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s,
                                     const PushEntry* push, int parts) {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
@@ -916,8 +926,8 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
   }
   if (parts & 2) {
     PhaseScope ph(PH_STAGE2, s);
-    stage_fused_kernel<NB, 2, S, 0, 2, true, SCH, 0><<<nslots * S, Geo<NB, 2, S, 0>::NT, Geo<NB, 2, S, 0>::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, push, hnbr, nullptr);
+    stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0><<<nslots * S, Geo<NB, 2, S, 0>::NT, Geo<NB, 2, S, 0>::SMEM, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr, nullptr);
     count_launch();
     *nrecords = (long long)nslots * S;
   }
@@ -959,11 +969,11 @@ static cudaError_t preload_nb() {
   }                                                                                                              \
   cudaError_t fused_hybrid_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,              \
                                           const SlotInfo* slots, const int* smap, int nbnd, int nint,            \
-                                          const PushEntry* hpush, const NbrEntry* nbr, const NbrEntry* hnbr,     \
+                                          const PushEntry* hpush, const NbrEntry* nbr,                           \
                                           const double* d_dt, double h_dt, DtRecord* records,                    \
                                           long long* nrecords, DevStatus* st, cudaStream_t s,                    \
                                           const PushEntry* push, int parts) {                                    \
-    return launch_hybrid_nb<NB, SCH>(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, hnbr, d_dt, h_dt, \
+    return launch_hybrid_nb<NB, SCH>(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, d_dt, h_dt,       \
                                      records, nrecords, st, s, push, parts);                                      \
   }
 

@@ -17,7 +17,7 @@ namespace orcha {
   cudaError_t fused_preload_n##NB##_s##SCH();                                                                   \
   cudaError_t fused_hybrid_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,              \
                                           const SlotInfo* slots, const int* smap, int nbnd, int nint,            \
-                                          const PushEntry* hpush, const NbrEntry* nbr, const NbrEntry* hnbr,     \
+                                          const PushEntry* hpush, const NbrEntry* nbr,                           \
                                           const double* d_dt, double h_dt, DtRecord* records,                    \
                                           long long* nrecords, DevStatus* st, cudaStream_t s,                    \
                                           const PushEntry* push, int parts);
@@ -78,12 +78,12 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
 // the self sides smap names.  Fused 3D shapes only (fused_supported).
 cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                   const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
-                                  const NbrEntry* hnbr, const double* d_dt, double h_dt, DtRecord* records,
+                                  const double* d_dt, double h_dt, DtRecord* records,
                                   long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                   int parts) {
   const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
 #define ORCHA_HYB(NB, SCH)                                                                                  \
-  fused_hybrid_n##NB##_s##SCH(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, hnbr, d_dt, h_dt, \
+  fused_hybrid_n##NB##_s##SCH(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, d_dt, h_dt,       \
                               records, nrecords, st, s, push, parts)
   if (G.nb[0] == 16) return var ? ORCHA_HYB(16, 1) : ORCHA_HYB(16, 0);
   if (G.nb[0] == 32) return var ? ORCHA_HYB(32, 1) : ORCHA_HYB(32, 0);

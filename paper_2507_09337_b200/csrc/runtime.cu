@@ -70,7 +70,7 @@ cudaError_t fused_preload(const DevGrid& G);
 long long fused_u1_cube(int nb);
 cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                                   const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
-                                  const NbrEntry* hnbr, const double* d_dt, double h_dt, DtRecord* records,
+                                  const double* d_dt, double h_dt, DtRecord* records,
                                   long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                   int parts);
 }  // namespace orcha
@@ -249,11 +249,10 @@ struct FillPlan {
   long long nslots_total = 0;
   // borrowed-ring telescoped step (one packet, not peer mode; fused_impl.cuh
   // launch_hybrid_nb): the slot map (slots with a self side first, each entry
-  // slot | self-side mask << 26), the x-ring push table and the U1 row table
+  // slot | self-side mask << 26) and the ring push table (face directions)
   int* d_hyb_smap = nullptr;
   int hyb_nbnd = 0, hyb_nint = 0;
   PushEntry* d_hyb_push = nullptr;
-  NbrEntry* d_hyb_nbr = nullptr;
 };
 // Frees a plan's device tables and the plan (not its packets' pointers).
 static void free_plan_tables(FillPlan* f) {
@@ -267,7 +266,6 @@ static void free_plan_tables(FillPlan* f) {
   cudaFree(f->d_sf_u1);
   cudaFree(f->d_hyb_smap);
   cudaFree(f->d_hyb_push);
-  cudaFree(f->d_hyb_nbr);
   delete f;
 }
 
@@ -758,7 +756,7 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     f->d_cross.push_back(dx);
     f->d_cross_u1.push_back(dx1);
   }
-  if (npk == 1 && !peer && fused_supported(G)) {
+  if (npk == 1 && !peer && fused_supported(G) && pk[0]->nslots < (1 << 26)) {
     // borrowed-ring telescoped step: a side of a block is "self" when its
     // neighbour is not a resident block of this packet reached by a shift
     // (physical boundary: clamp / mirror; another rank or packet) -- there
@@ -767,7 +765,6 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     const long long U1C = fused_u1_cube(G.nb[0]);
     std::vector<int> bnd, inr;
     std::vector<PushEntry> hp((size_t)p->nslots * 27, PushEntry{nullptr, 0, 0});
-    std::vector<NbrEntry> hn((size_t)p->nslots * 27, NbrEntry{nullptr, 0, 0});
     auto local_slot = [&](const int bc[3], const int o[3], int* mode) -> int {
       HostEntry h = make_entry(g, bc, o);
       *mode = h.mode;
@@ -787,17 +784,8 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
           o[a] = sd ? 1 : -1;
           const int ns = local_slot(bc, o, &md);
           if (ns < 0) mask |= 1 << (2 * a + sd);
-          else if (a == 0) hp[(size_t)s * 27 + (sd ? 14 : 12)] = PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
-        }
-      for (int oz = -1; oz <= 1; oz++)
-        for (int oy = -1; oy <= 1; oy++) {
-          if (oy == 0 && oz == 0) continue;
-          const bool self = (oy != 0 && ((mask >> (2 + (oy > 0))) & 1)) || (oz != 0 && ((mask >> (4 + (oz > 0))) & 1));
-          int o[3] = {0, oy, oz};
-          const int ns = self ? -1 : local_slot(bc, o, &md);
-          if (ns >= 0)
-            hn[(size_t)s * 27 + (oz + 1) * 9 + (oy + 1) * 3 + 1] =
-                NbrEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
+          else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
+                   PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
         }
       (mask ? bnd : inr).push_back(s | (mask << 26));
     }
@@ -811,9 +799,6 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     if (err == cudaSuccess) err = cudaMalloc(&f->d_hyb_push, hp.size() * sizeof(PushEntry));
     if (err == cudaSuccess)
       err = cudaMemcpy(f->d_hyb_push, hp.data(), hp.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMalloc(&f->d_hyb_nbr, hn.size() * sizeof(NbrEntry));
-    if (err == cudaSuccess)
-      err = cudaMemcpy(f->d_hyb_nbr, hn.data(), hn.size() * sizeof(NbrEntry), cudaMemcpyHostToDevice);
     if (err != cudaSuccess) {
       free_plan_tables(f);
       return cuda_fail(err, "upload borrowed-ring tables");
@@ -1202,7 +1187,7 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
            p->d_nbr == p->push_plan->d_tables[0])
     e = launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, p->push_plan->d_hyb_smap,
                               p->push_plan->hyb_nbnd, p->push_plan->hyb_nint, p->push_plan->d_hyb_push, p->d_nbr,
-                              p->push_plan->d_hyb_nbr, d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3);
+                              d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3);
   else if (!p->peer_comm)
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                              &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr, xpush);

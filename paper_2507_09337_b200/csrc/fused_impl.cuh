@@ -105,6 +105,11 @@
 #define ORCHA_XSHFL 0
 #endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
+// 4-deep staging ring for the kernels with the z-face carry (its z-faces
+// never read the plane below the output plane after the prologue)
+#ifndef ORCHA_RING4
+#define ORCHA_RING4 1
+#endif
 #ifndef ORCHA_ISSUE_LAST
 #define ORCHA_ISSUE_LAST 0
 #endif
@@ -164,7 +169,15 @@ struct Geo {
   static constexpr int H = W / NSPLIT;                       // output rows per CTA
   static constexpr int IR = H + 4;                           // staged input rows per plane
   static constexpr int BAND = IR * IPX;                      // doubles per staged band per variable
-  static constexpr int NS = 5;                               // ring depth
+  // z-face carry (see ORCHA_ZCARRY): bit 0 stage 1 of both methods, bit 1 the
+  // telescoped stage 2, bit 2 the per-stage variant's stage 2; not for 8^3
+  // blocks, whose stage 1 fits 3 CTAs per SM without it and 2 with (measured:
+  // 3.09 -> 2.59 G cu/s for one packet)
+  static constexpr bool ZC = ((ORCHA_ZCARRY >> (STAGE == 1 ? 0 : MODE == 1 ? 2 : 1)) & 1) && NB >= 16;
+  // ring depth: the faces of output plane k read staged planes k-1 .. k+2
+  // (k .. k+2 with the z-face carry) while plane k+3 is converted and the
+  // copy of the next one lands -- 5 slots, 4 with the carry (ORCHA_RING4)
+  static constexpr int NS = (ZC && ORCHA_RING4) ? 4 : 5;
   static constexpr int FX = H * (W + 1);                     // x-faces per band
   static constexpr int FY = (H + 1) * W;                     // y-faces per band
   static constexpr int FZ = H * W;                           // z-faces per band (and cells)
@@ -187,11 +200,6 @@ struct Geo {
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
-  // z-face carry slots; not for 8^3 blocks, whose stage 1 fits 3 CTAs per SM
-  // without them and 2 with (measured: 3.09 -> 2.59 G cu/s for one packet)
-  // (bit 0: stage 1 of both methods; bit 1: the telescoped stage 2; bit 2:
-  // the per-stage variant's stage 2)
-  static constexpr bool ZC = ((ORCHA_ZCARRY >> (STAGE == 1 ? 0 : MODE == 1 ? 2 : 1)) & 1) && NB >= 16;
   static constexpr size_t SMEM =
       sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ + (ZC ? 5 * FZ : 0)) + 64 +
       ((NS * IR + 15) / 16) * 16;
@@ -561,14 +569,21 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   if (issuer)
     for (int p = 0; p < NS; p++) issue(p);
   if (GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
-  for (int p = 0; p < 5; p++) {
+  for (int p = 0; p < NS; p++) {
     wait_plane(p);
     convert(p);
   }
   __syncthreads();
   for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
   __syncthreads();
-  if (issuer) issue(5);  // into the slot of plane 0
+  if (issuer)  // into the slots of planes 0 (and 1: a 4-deep ring, dead once the prologue faces are done)
+    for (int p = NS; p < 6; p++) issue(p);
+  if (NS == 4) {  // plane 4 is read by the first output plane's z-faces
+    if (GATHER) __syncthreads();  // its sign-flip masks
+    wait_plane(4);
+    convert(4);
+    __syncthreads();
+  }
 
   double s_rec = -DBL_MAX;
   long long g_rec = LLONG_MAX;

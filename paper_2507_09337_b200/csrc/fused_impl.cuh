@@ -316,6 +316,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const long long slot = HYB ? (me & 0x3ffffff) : me;
   const int selfm = HYB ? ((me >> 26) & 63) : 0;  // self-ring sides: bit 2a (-a), 2a+1 (+a)
   const int band = blockIdx.x % Gm::NSPLIT;
+  // output planes [kz0, kz0 + nk): the geometry's, or (HYB stage 1) the
+  // interior extended by the 2 ring planes on the self z sides only
+  const int zlo = (HYB && STAGE == 1) ? ((selfm >> 4) & 1) * 2 : Gm::OFF;
+  const int zhi = (HYB && STAGE == 1) ? ((selfm >> 5) & 1) * 2 : Gm::OFF;
+  const int kz0 = -zlo, nk = NB + zlo + zhi, nplanes = nk + 4;
+  const int porg = INO - 2 - zlo;  // padded plane of staged plane 0
   const int jj0 = band * H;                              // first output row of the band (0-based)
   const long long cube = G.cube;
   const double dt = d_dt ? *d_dt : h_dt;
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   // generic access to the slot; the proxy fence of each issuing lane orders
   // those before its async copies.
   auto issue = [&](int p) {
-    if (p < Gm::NPLANES) {
+    if (p < nplanes) {
       const int s = p % NS, lane = tid & 31;
       if (GATHER) {
         // Gather mode: only the x-guards were filled.  Each staged row
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         // the fly (x, then y over x-guards, then z over x,y-guards).  Lane r
         // resolves row r; rows whose sources are consecutive form one copy,
         // issued by the lane that starts the run.
-        const int pp = p + ORG, z = pp - INO;
+        const int pp = p + porg, z = pp - INO;
         const int oz = z < 0 ? -1 : (z >= NB ? 1 : 0);
         const double* rp = nullptr;
         int fl = 0;
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 #pragma unroll
         for (int v = 0; v < 5; v++)
           bulk_load(ring + (s * 5 + v) * BAND,
-                    in + v * in_cube + (long long)(p + ORG) * Gm::PLANE + (long long)(jj0 + ORG) * IPX, BAND * 8u,
+                    in + v * in_cube + (long long)(p + porg) * Gm::PLANE + (long long)(jj0 + ORG) * IPX, BAND * 8u,
                     &bar[s]);
       }
     }
@@ -403,7 +409,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   // EOS in place over the staged band of plane p: cells c0, c0 + nthr, ...
   auto convert = [&](int p, int c0 = -1, int nthr = Gm::NT) {
     double* Q = ring + (p % NS) * 5 * BAND;
-    const int z = Gm::K0 - 2 + p;
+    const int z = kz0 - 2 + p;
     unsigned long long hits = 0;
     for (int c = (c0 < 0 ? tid : c0); c < BAND; c += nthr) {
       bool fl;
@@ -588,8 +594,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   double s_rec = -DBL_MAX;
   long long g_rec = LLONG_MAX;
 #pragma unroll 1
-  for (int it = 0; it < Gm::NK; it++) {
-    const int k = Gm::K0 + it;
+  for (int it = 0; it < nk; it++) {
+    const int k = kz0 + it;
     // prefetch the update operands of this thread's cell of plane k
     const bool upd = tid < Gm::FZ;
     const int lj = upd ? tid / W : 0, li = upd ? tid - (tid / W) * W : 0;
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       const double* ub = state + slot * 5 * cube;
       long long uo = so;
       int ufl = 0;
-      if (STAGE == 1 && MODE == 0 && GATHER) {
+      if (STAGE == 1 && (MODE == 0 || HYB) && GATHER) {
         // gather mode: the box's y/z guard-ring cells were not filled; U^n of
         // such a cell is its image in the owning block (x-guards are filled)
         const int oy = cj < 0 ? -1 : (cj >= NB ? 1 : 0), oz = k < 0 ? -1 : (k >= NB ? 1 : 0);
@@ -639,7 +645,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     // the EOS of plane it+5 (read from iteration it+1 on; its copy was issued
     // one plane earlier): ORCHA_ONEBAR before the barrier, else after it
     auto convert_next = [&]() {
-      if (it + 5 < Gm::NPLANES) {
+      if (it + 5 < nplanes) {
         if constexpr (CSPLIT) {
           if (warp >= UW) {
             wait_plane(it + 5);
@@ -893,13 +899,17 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
 // physical boundary (the ring is U1 of the BC-imaged U^n, which no block
 // owns) or an owner on another rank (no second exchange) -- need the ring
 // computed.  So stage 1 runs in two launches over the slot map:
-//   smap[0, nbnd):        blocks with a self side, the box kernel (MODE 0
-//                         geometry), ring cells stored on self sides only;
-//   smap[nbnd, +nint):    the rest, interior only (MODE 1 geometry);
-// both write U1 into the compact (n+4)^3 cubes and push their 2-cell
-// boundary layers into the ring of the face neighbours' cubes (hpush), so
-// stage 2 is the plain telescoped stage-2 kernel over complete cubes.  Stage-1 work per block: 1x
-// instead of (n+4)^3/n^3 (1.95x at 16^3, 3.4x at 8^3) away from self sides.
+//   smap[0, nbnd):        blocks with an x or y self side: the box kernel
+//                         (MODE 0 geometry: 20 x 20 output columns of 16^3);
+//   smap[nbnd, +nint):    the rest: the interior kernel (MODE 1 geometry);
+// in both the output planes are the interior plus the 2 ring planes on the
+// self z sides only (runtime plane range), and ring cells are stored on
+// self sides only.  Both write U1 into the compact (n+4)^3 cubes and push
+// their 2-cell boundary layers into the ring of the face neighbours' cubes
+// (hpush), so stage 2 is the plain telescoped stage-2 kernel over complete
+// cubes.  Stage-1 cell-stages per cell-update on cfg4 (16^3 blocks, 16^3
+// of them, outflow): 1.95 computed ring, 1.15 borrowed (1.0 away from self
+// sides; 3.4 -> 1.0 at 8^3).
 template <int NB, int SCH>
 static cudaError_t hybrid_attrs() {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;

@@ -787,7 +787,9 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
           else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
                    PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
         }
-      (mask ? bnd : inr).push_back(s | (mask << 26));
+      // x / y self sides: the box kernel; none, or z only: the interior
+      // kernel (its plane range extended on the self z sides)
+      ((mask & 15) ? bnd : inr).push_back(s | (mask << 26));
     }
     std::vector<int> smap = bnd;
     smap.insert(smap.end(), inr.begin(), inr.end());

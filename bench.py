@@ -51,12 +51,59 @@ def algorithmic_costs(nb=16, ng=4, fill_mode="gather"):
     return adv_bytes, fill_bytes, FP64_INSTR_PER_CU
 
 
-FP64_INSTR_PER_CU = 1498.0
-# executed thread-instructions per cell-update of the two stage kernels (ncu
-# source page of the current kernels; profiles/r02_sass_mix_v16.txt) -- the
-# issue-slot view of the same kernels (context beside the fp64 roofline)
-EXEC_INSTR_PER_CU = 3758.0
-EXEC_INSTR_SOURCE = "profiles/r02_sass_mix_v16.txt"
+FP64_INSTR_PER_CU = 1498.0   # the literal telescoped step (computed ring on every side), SURVEY 8(d)
+# fp64-pipe work model of one step: 142 per face flux (slopes
+# shared), 15 per EOS cell (A5), FP64_PER_UPDATE per updated
+# cell -- the last calibrated so that the literal telescoped 16^3 step is
+# SURVEY's 1498 per cell-update (its F1 row then comes out at 1026 vs 1033)
+FP64_PER_FACE, FP64_PER_EOS = 142.0, 15.0
+# executed thread-instructions per cell-update of the advance kernels (ncu
+# source page of the current kernels) -- the issue-slot view of the same
+# kernels (context beside the fp64 roofline)
+EXEC_INSTR_PER_CU = 2963.7
+EXEC_INSTR_SOURCE = "profiles/r02_sass_mix_ring_v4.txt"
+
+
+def _stage_counts(w):
+    wx, wy, wz = w
+    faces = (wx + 1) * wy * wz + wx * (wy + 1) * wz + wx * wy * (wz + 1)
+    return faces, (wx + 4) * (wy + 4) * (wz + 4), wx * wy * wz
+
+
+def _fp64_per_update(nb=16):
+    f1, e1, u1 = _stage_counts((nb + 4,) * 3)
+    f2, e2, u2 = _stage_counts((nb,) * 3)
+    return (FP64_INSTR_PER_CU * nb ** 3 - FP64_PER_FACE * (f1 + f2) - FP64_PER_EOS * (e1 + e2)) / (u1 + u2)
+
+
+def step_fp64_model(stage1_regions, nb=16):
+    """Algorithmic fp64-pipe instructions per cell-update of a step whose
+    stage 1 covers the given per-block output regions (wx, wy, wz) and whose
+    stage 2 covers each block's interior."""
+    per_u = _fp64_per_update(nb)
+    tot = 0.0
+    for w in stage1_regions + [(nb,) * 3] * len(stage1_regions):
+        f, e, c = _stage_counts(w)
+        tot += FP64_PER_FACE * f + FP64_PER_EOS * e + per_u * c
+    return tot / (len(stage1_regions) * nb ** 3)
+
+
+def borrowed_ring_regions(brick, nb=16):
+    """Stage-1 output region of each block of a rank's brick under the
+    borrowed ring (include/orcha.h orcha_set_ring_mode): self sides are the
+    brick faces (a physical boundary or another rank); blocks with an x or y
+    self side run the box kernel (20 x 20 columns), the rest the interior
+    kernel; both extend the planes by 2 on each self z side."""
+    out = []
+    for k in range(brick[2]):
+        for j in range(brick[1]):
+            for i in range(brick[0]):
+                sx = (i == 0) + (i == brick[0] - 1)
+                sy = (j == 0) + (j == brick[1] - 1)
+                sz = (k == 0) + (k == brick[2] - 1)
+                w = nb + 4 if (sx or sy) else nb
+                out.append((w, w, nb + 2 * sz))
+    return out
 
 
 def measured_traffic():
@@ -721,6 +768,12 @@ def main():
     # the local part of the fill follows the mode)
     fill_eff = args.fill_mode
     adv_bytes, fill_bytes, fp_instr = algorithmic_costs(fill_mode=fill_eff)
+    # the borrowed ring (default: gather fill, one packet, not F2 peer mode)
+    # computes the stage-1 ring on the brick faces only: its own work model
+    borrowed = (lib.orcha_get_ring_mode() == 1 and args.fill_mode == "gather" and args.method == "telescoped"
+                and not (args.comm == "ipc" and world > 1))
+    regions = borrowed_ring_regions(BRICK_BLOCKS, NB[0]) if borrowed else [(NB[0] + 4,) * 3]
+    fp_instr = step_fp64_model(regions, NB[0])
     cu_local = BRICK_BLOCKS[0] * BRICK_BLOCKS[1] * BRICK_BLOCKS[2] * NB[0] * NB[1] * NB[2]
     hbm_achieved = adv_bytes * cu_local / (adv_ms / 1e3) / 1e9
     fp_achieved = fp_instr * cu_local / (adv_ms / 1e3) / 1e12
@@ -734,8 +787,17 @@ def main():
                "traffic_source": traffic_src,
                "peak_source": "derived (DESIGN.md 6): 148 SM x 64 fp64 lanes x sm_max clock",
                "peak_measured": fp64_probe["tinst_per_s"] if fp64_probe else None,
-               "kernel": "hydro_advance (stage_fused_kernel<16,1> + <16,2>)",
-               "algorithmic_fp64_instr_per_cell_update": fp_instr, "units_per_launch": cu_local}
+               "kernel": "hydro_advance (stage_fused_kernel<16,1> box + interior, <16,2>)",
+               "algorithmic_fp64_instr_per_cell_update": fp_instr, "units_per_launch": cu_local,
+               "ring": "borrowed" if borrowed else "computed",
+               "work_model": "142 fp64 per face + 15 per EOS cell + 31.1 per updated cell over the step's "
+                             "stage-1 / stage-2 regions (DESIGN.md 6)",
+               "literal_telescoped_equivalent": {
+                   "fp64_instr_per_cell_update": FP64_INSTR_PER_CU,
+                   "achieved": FP64_INSTR_PER_CU * cu_local / (adv_ms / 1e3) / 1e12,
+                   "frac": FP64_INSTR_PER_CU * cu_local / (adv_ms / 1e3) / 1e12 / pks["fp64_tinst"],
+                   "note": "the literal step's work (ring computed on every side) per second of this advance: "
+                           "context, not the kernel's own efficiency"}}
     primary, other = (roof_fp, roof_hbm) if roof_fp["frac"] >= roof_hbm["frac"] else (roof_hbm, roof_fp)
     # issue slots: 148 SMs x 4 schedulers x 1 warp-instruction per cycle
     issue_peak = 148 * 4 * pks.get("sm_max_mhz", 1965.0) * 1e6 * 32 / 1e12   # T thread-instructions/s

@@ -43,6 +43,9 @@
 #ifndef ORCHA_CONV_SPLIT
 #define ORCHA_CONV_SPLIT 1
 #endif
+#ifndef ORCHA_CONV_BAL
+#define ORCHA_CONV_BAL 1
+#endif
 // face-task rounds per warp (16^3 / 32^3): stage 1 (and both per-stage
 // stages, and 32^3 blocks) / telescoped 16^3 stage 2 (3: 5-warp CTAs, 3 per
 // SM; measured best -- 32^3 stage 2 is faster with 2: 5.57 vs 5.36 G)
@@ -88,13 +91,14 @@
 #define ORCHA_ONEBAR 0
 #endif
 // z-face carry (ORCHA_ZCARRY: bit 0 stage 1, bit 1 telescoped stage 2, bit 2
-// per-stage stage 2; only bit 0 measured faster -- profiles/r02_ab_zcarry*.txt): the
+// per-stage stage 2; bits 0 and 1 measured faster, bit 1 only with the 4-deep
+// ring -- profiles/r02_ab_zcarry*.txt, r02_ab_ring4_zc3.txt): the
 // z-face task of a column computes the z-slope of cell k+1 once and keeps
 // its upper face state q + s/2 (the left state of face k+3/2) in a
 // per-column shared slot for the next plane, instead of recomputing that
 // slope there (one slope per z-face instead of two; bitwise the same values)
 #ifndef ORCHA_ZCARRY
-#define ORCHA_ZCARRY 1
+#define ORCHA_ZCARRY 3
 #endif
 // x-face slope sharing (ORCHA_XSHFL): an x-face slot deals CELLS to lanes
 // (31 new ones per warp, one overlap lane); each lane computes its cell's
@@ -340,6 +344,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   uint64_t* fdone = &bar[NS];  // ORCHA_ONEBAR: the update warps have read the face arrays of the plane
   uint64_t* cdone = &bar[NS + 1];  // ORCHA_ONEBAR 2: the converting warps have converted plane it+5
   constexpr bool CSPLIT = ORCHA_CONV_SPLIT && Gm::NW - UWARPS >= 2;
+  // ORCHA_CONV_BAL: the converting warps take 2 rounds of 32 cells each and
+  // the update warps the rest after their update (one round each when the
+  // band is small enough), instead of the converting warps taking all of it
+  // (3 rounds in both stage-1 kernels against one update)
+  constexpr int CONV_END = (CSPLIT && ORCHA_CONV_BAL && 2 * (Gm::NW - UWARPS) * 32 < BAND)
+                               ? 2 * (Gm::NW - UWARPS) * 32 : BAND;
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     mbar_init(fdone, UWARPS);
@@ -407,11 +417,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   };
   auto wait_plane = [&](int p) { mbar_wait(&bar[p % NS], (p / NS) & 1); };
   // EOS in place over the staged band of plane p: cells c0, c0 + nthr, ...
-  auto convert = [&](int p, int c0 = -1, int nthr = Gm::NT) {
+  auto convert = [&](int p, int c0 = -1, int nthr = Gm::NT, int cend = Gm::BAND) {
     double* Q = ring + (p % NS) * 5 * BAND;
     const int z = kz0 - 2 + p;
     unsigned long long hits = 0;
-    for (int c = (c0 < 0 ? tid : c0); c < BAND; c += nthr) {
+    for (int c = (c0 < 0 ? tid : c0); c < cend; c += nthr) {
       bool fl;
       int r = c / IPX;
       double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
@@ -649,7 +659,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         if constexpr (CSPLIT) {
           if (warp >= UW) {
             wait_plane(it + 5);
-            convert(it + 5, tid - UW * 32, NT - UW * 32);
+            convert(it + 5, tid - UW * 32, NT - UW * 32, CONV_END);
           }
         } else {
           wait_plane(it + 5);
@@ -732,6 +742,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         bool finite = isfinite(nw[0]) && isfinite(nw[1]) && isfinite(nw[2]) && isfinite(nw[3]) && isfinite(nw[4]);
         if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)g);
       }
+      }
+    }
+    if constexpr (CONV_END < BAND) {  // the update warps' share of the next plane's EOS
+      if (warp < UWARPS && it + 5 < nplanes) {
+        wait_plane(it + 5);
+        convert(it + 5, CONV_END + tid, UWARPS * 32, BAND);
       }
     }
     if (!ORCHA_ONEBAR) __syncthreads();

@@ -44,7 +44,7 @@
 #define ORCHA_CONV_SPLIT 1
 #endif
 #ifndef ORCHA_CONV_BAL
-#define ORCHA_CONV_BAL 1
+#define ORCHA_CONV_BAL 0
 #endif
 // face-task rounds per warp (16^3 / 32^3): stage 1 (and both per-stage
 // stages, and 32^3 blocks) / telescoped 16^3 stage 2 (3: 5-warp CTAs, 3 per
@@ -347,7 +347,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   // ORCHA_CONV_BAL: the converting warps take 2 rounds of 32 cells each and
   // the update warps the rest after their update (one round each when the
   // band is small enough), instead of the converting warps taking all of it
-  // (3 rounds in both stage-1 kernels against one update)
+  // (3 rounds in both stage-1 kernels against one update).  Measured slower
+  // (2.46 vs 2.40 ms per cfg4 step, profiles/r02_ab_convbal.txt): off
   constexpr int CONV_END = (CSPLIT && ORCHA_CONV_BAL && 2 * (Gm::NW - UWARPS) * 32 < BAND)
                                ? 2 * (Gm::NW - UWARPS) * 32 : BAND;
   if (tid == 0) {

@@ -949,21 +949,36 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
                                     const int* smap, int nbnd, int nint, const PushEntry* hpush,
                                     const NbrEntry* nbr, const double* d_dt, double h_dt,
                                     DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s,
-                                    const PushEntry* push, int parts) {
+                                    const PushEntry* push, int parts, cudaStream_t side, cudaEvent_t ev_fork,
+                                    cudaEvent_t ev_join) {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
   cudaError_t e = hybrid_attrs<NB, SCH>();
   if (e != cudaSuccess) return e;
   if (parts & 1) {
     PhaseScope ph(PH_STAGE1, s);
+    // side stream (optional): the box kernel runs beside the interior one
+    // (they read only U^n and write disjoint cells), filling each other's tail
+    const bool fork = side != nullptr && nbnd > 0 && nint > 0;
+    if (fork) {
+      e = cudaEventRecord(ev_fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork, 0);
+      if (e != cudaSuccess) return e;
+    }
     if (nbnd > 0) {
-      stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1><<<nbnd * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap);
+      stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>
+          <<<nbnd * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM, fork ? side : s>>>(
+              G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap);
       count_launch();
     }
     if (nint > 0) {
       stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM, s>>>(
           G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap + nbnd);
       count_launch();
+    }
+    if (fork) {
+      e = cudaEventRecord(ev_join, side);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_join, 0);
+      if (e != cudaSuccess) return e;
     }
   }
   if (parts & 2) {
@@ -1014,9 +1029,10 @@ static cudaError_t preload_nb() {
                                           const PushEntry* hpush, const NbrEntry* nbr,                           \
                                           const double* d_dt, double h_dt, DtRecord* records,                    \
                                           long long* nrecords, DevStatus* st, cudaStream_t s,                    \
-                                          const PushEntry* push, int parts) {                                    \
+                                          const PushEntry* push, int parts, cudaStream_t side,                   \
+                                          cudaEvent_t ev_fork, cudaEvent_t ev_join) {                            \
     return launch_hybrid_nb<NB, SCH>(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, d_dt, h_dt,       \
-                                     records, nrecords, st, s, push, parts);                                      \
+                                     records, nrecords, st, s, push, parts, side, ev_fork, ev_join);              \
   }
 
 }  // namespace orcha

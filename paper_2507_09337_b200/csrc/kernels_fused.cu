@@ -20,7 +20,8 @@ namespace orcha {
                                           const PushEntry* hpush, const NbrEntry* nbr,                           \
                                           const double* d_dt, double h_dt, DtRecord* records,                    \
                                           long long* nrecords, DevStatus* st, cudaStream_t s,                    \
-                                          const PushEntry* push, int parts);
+                                          const PushEntry* push, int parts, cudaStream_t side,                   \
+                                          cudaEvent_t ev_fork, cudaEvent_t ev_join);
 ORCHA_FUSED_DECL(8, 0)
 ORCHA_FUSED_DECL(8, 1)
 ORCHA_FUSED_DECL(16, 0)
@@ -80,11 +81,11 @@ cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, i
                                   const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
                                   const double* d_dt, double h_dt, DtRecord* records,
                                   long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
-                                  int parts) {
+                                  int parts, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
   const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
 #define ORCHA_HYB(NB, SCH)                                                                                  \
   fused_hybrid_n##NB##_s##SCH(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, d_dt, h_dt,       \
-                              records, nrecords, st, s, push, parts)
+                              records, nrecords, st, s, push, parts, side, ev_fork, ev_join)
   if (G.nb[0] == 16) return var ? ORCHA_HYB(16, 1) : ORCHA_HYB(16, 0);
   if (G.nb[0] == 32) return var ? ORCHA_HYB(32, 1) : ORCHA_HYB(32, 0);
   return var ? ORCHA_HYB(8, 1) : ORCHA_HYB(8, 0);

@@ -72,7 +72,7 @@ cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, i
                                   const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
                                   const double* d_dt, double h_dt, DtRecord* records,
                                   long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
-                                  int parts);
+                                  int parts, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
 }  // namespace orcha
 
 // Fill mode: 1 = gather (default): when every guard source of the packet set
@@ -1166,6 +1166,23 @@ extern "C" int32_t orcha_comm_push_dt(orcha_comm* comm, orcha_packet* const* pk,
 }
 
 // ----------------------------------------------------------- advance -----
+// Borrowed ring: the box and interior stage-1 kernels on two streams
+// (ORCHA_HYB_CONC=0: one after the other on the caller's stream).
+static bool hyb_concurrent() {
+  static const bool on = [] {
+    const char* e = getenv("ORCHA_HYB_CONC");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+static cudaError_t hyb_side(orcha_packet* p) {
+  if (!hyb_concurrent() || p->side) return cudaSuccess;
+  cudaError_t e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_halo, cudaEventDisableTiming);
+  return e;
+}
+
 static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, void* stream) {
   if (!p) return fail(ORCHA_E_ARG, "null packet");
   if (!p->guards_valid || !p->guards_full)
@@ -1186,10 +1203,11 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
   else if (!p->peer_comm && xpush && ring_mode() == 1 && p->push_plan->d_hyb_smap &&
-           p->d_nbr == p->push_plan->d_tables[0])
+           p->d_nbr == p->push_plan->d_tables[0] && (e = hyb_side(p)) == cudaSuccess)
     e = launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, p->push_plan->d_hyb_smap,
                               p->push_plan->hyb_nbnd, p->push_plan->hyb_nint, p->push_plan->d_hyb_push, p->d_nbr,
-                              d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3);
+                              d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3,
+                              hyb_concurrent() ? p->side : nullptr, p->ev_ready, p->ev_halo);
   else if (!p->peer_comm)
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                              &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr, xpush);

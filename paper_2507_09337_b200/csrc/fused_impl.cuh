@@ -227,6 +227,20 @@ __device__ __forceinline__ int guard_image(int c, int o, int m) {
   return o == 0 ? c : m == kShift ? c - o * NB : m == kClamp ? (o < 0 ? 0 : NB - 1) : (o < 0 ? -1 - c : 2 * NB - 1 - c);
 }
 
+// The fused kernels' padded block geometry is known at compile time (ng = 4,
+// fused_supported): in-cube offsets in 32-bit arithmetic with constant
+// strides instead of cell_off's 64-bit products of DevGrid fields (measured:
+// ~50 integer instructions per cell-update of stage 2 went to those).
+template <int NB>
+__host__ __device__ constexpr int cube_c() {
+  return (int)((((long long)(NB + 8) * (NB + 8) * (NB + 8) * 8 + (long long)kAlign - 1) / (long long)kAlign *
+                (long long)kAlign) / 8);
+}
+template <int NB>
+__device__ __forceinline__ int coff(int i, int j, int k) {
+  return ((k + 4) * (NB + 8) + (j + 4)) * (NB + 8) + (i + 4);
+}
+
 // U1 scratch of the fused path: per (slot, var) an (n+4)^3 cube (origin -2),
 // 256-byte aligned.
 template <int NB>
@@ -249,9 +263,9 @@ __device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, i
   else if (m == kMirror) t0 = side ? 2 * NB - 1 - ci : -1 - ci;
   else { cnt = (side ? ci == NB - 1 : ci == 0) ? 4 : 0; t0 = side ? NB : -4; }
   for (int xx = 0; xx < cnt; xx++) {
-    double* q = e.dst + cell_off(G, t0 + xx, cj, k);
+    double* q = e.dst + coff<NB>(t0 + xx, cj, k);
 #pragma unroll
-    for (int v = 0; v < 5; v++) q[v * G.cube] = ((e.flip >> v) & 1) ? -w[v] : w[v];
+    for (int v = 0; v < 5; v++) q[v * cube_c<NB>()] = ((e.flip >> v) & 1) ? -w[v] : w[v];
   }
 }
 
@@ -263,7 +277,7 @@ __device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, i
 // edge feeds each face neighbour separately (edge cells of the ring are read
 // by no stage-2 stencil).
 template <int NB>
-__device__ __forceinline__ void push_u1(const PushEntry* sxp, long long U1C, int ci, int cj, int k,
+__device__ __forceinline__ void push_u1(const PushEntry* sxp, int U1C, int ci, int cj, int k,
                                         const double w[5]) {
   if (ci < 0 || ci >= NB || cj < 0 || cj >= NB || k < 0 || k >= NB) return;
   const int c[3] = {ci, cj, k};
@@ -275,7 +289,7 @@ __device__ __forceinline__ void push_u1(const PushEntry* sxp, long long U1C, int
     if (d == nullptr) continue;
     int t[3] = {ci, cj, k};
     t[a] = side ? c[a] - NB : c[a] + NB;
-    double* q = d + ((long long)(t[2] + 2) * (NB + 4) + (t[1] + 2)) * (NB + 4) + (t[0] + 2);
+    double* q = d + ((t[2] + 2) * (NB + 4) + (t[1] + 2)) * (NB + 4) + (t[0] + 2);
 #pragma unroll
     for (int v = 0; v < 5; v++) q[v * U1C] = w[v];
   }
@@ -302,9 +316,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   // U1 cube stride: (n+4)^3 compact scratch (telescoped, and every hybrid
   // kernel) or the padded state layout (per-stage)
   constexpr bool CU1 = MODE == 0 || HYB;
-  const long long U1C = CU1 ? u1_cube<NB>() : G.cube;
-  auto u1_off = [&](int ci, int cj, int k) -> long long {
-    return CU1 ? ((long long)(k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2) : cell_off(G, ci, cj, k);
+  constexpr int U1C = CU1 ? (int)u1_cube<NB>() : cube_c<NB>();
+  auto u1_off = [&](int ci, int cj, int k) -> int {
+    return CU1 ? ((k + 2) * (NB + 4) + (cj + 2)) * (NB + 4) + (ci + 2) : coff<NB>(ci, cj, k);
   };
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;                                   // [NS][5][IR][IPX]
@@ -327,10 +341,10 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const int kz0 = -zlo, nk = NB + zlo + zhi, nplanes = nk + 4;
   const int porg = INO - 2 - zlo;  // padded plane of staged plane 0
   const int jj0 = band * H;                              // first output row of the band (0-based)
-  const long long cube = G.cube;
+  constexpr int cube = cube_c<NB>();  // == G.cube (checked at launch)
   const double dt = d_dt ? *d_dt : h_dt;
   const double* in = (STAGE == 1) ? state + slot * 5 * cube : u1 + slot * 5 * U1C;
-  const long long in_cube = (STAGE == 1) ? cube : U1C;
+  constexpr int in_cube = (STAGE == 1) ? cube : U1C;
   const SlotInfo si = slots[slot];
 
   // PUSH == 2: the -x / +x push targets of this block; HYB stage 1: the six
@@ -611,11 +625,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     const bool upd = tid < Gm::FZ;
     const int lj = upd ? tid / W : 0, li = upd ? tid - (tid / W) * W : 0;
     const int ci = li - OFF, cj = jj0 + lj - OFF;
-    const long long so = cell_off(G, ci, cj, k);
+    const int so = coff<NB>(ci, cj, k);
     double un[5], v1[5];
     if (upd) {
       const double* ub = state + slot * 5 * cube;
-      long long uo = so;
+      int uo = so;
       int ufl = 0;
       if (STAGE == 1 && (MODE == 0 || HYB) && GATHER) {
         // gather mode: the box's y/z guard-ring cells were not filled; U^n of
@@ -625,7 +639,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
           const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
           if (e.src != nullptr) {
             ub = e.src;
-            uo = cell_off(G, ci, guard_image<NB>(cj, oy, (e.mode >> 2) & 3), guard_image<NB>(k, oz, (e.mode >> 4) & 3));
+            uo = coff<NB>(ci, guard_image<NB>(cj, oy, (e.mode >> 2) & 3), guard_image<NB>(k, oz, (e.mode >> 4) & 3));
             ufl = e.flip & 0xC;
           }
         }
@@ -635,7 +649,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       if (ufl & 4) un[2] = -un[2];
       if (ufl & 8) un[3] = -un[3];
       if (STAGE == 2) {
-        const long long uo = u1_off(ci, cj, k);
+        const int uo = u1_off(ci, cj, k);
 #pragma unroll
         for (int v = 0; v < 5; v++) v1[v] = __ldg(u1 + slot * 5 * U1C + v * U1C + uo);
       }
@@ -844,6 +858,7 @@ template <int NB, int SCH>
 static cudaError_t launch_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
                              const double* d_dt, double h_dt, DtRecord* records, long long* nrecords, DevStatus* st,
                              cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk, int parts) {
+  if (G.cube != cube_c<NB>() || G.gd[0] != 4 || G.P[0] != NB + 8) return cudaErrorInvalidValue;  // compile-time geometry
   int s2 = 1;
   if constexpr (NB == 16) {
     static const int s1 = split_env("ORCHA_SPLIT1", 2);
@@ -896,6 +911,7 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
                                    long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                    const NbrEntry* nbr, int pk) {
   constexpr int SP = (NB == 16) ? 2 : (NB == 32) ? 4 : 1;
+  if (G.cube != cube_c<NB>() || G.gd[0] != 4 || G.P[0] != NB + 8) return cudaErrorInvalidValue;  // compile-time geometry
   PhaseScope ph(stage == 1 ? PH_STAGE1 : PH_STAGE2, s);
   if (stage == 1) {
     launch_stage<NB, 1, SP, 1, SCH>(G, state, u1, nslots, slots, d_dt, h_dt, records, st, s, push, nbr, pk);
@@ -952,6 +968,7 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
                                     const PushEntry* push, int parts, cudaStream_t side, cudaEvent_t ev_fork,
                                     cudaEvent_t ev_join) {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
+  if (G.cube != cube_c<NB>() || G.gd[0] != 4 || G.P[0] != NB + 8) return cudaErrorInvalidValue;
   cudaError_t e = hybrid_attrs<NB, SCH>();
   if (e != cudaSuccess) return e;
   if (parts & 1) {

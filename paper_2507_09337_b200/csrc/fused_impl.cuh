@@ -204,9 +204,14 @@ struct Geo {
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
+  // (+ the gather mode's per-row sources of the three z classes, 3 x IR x 16 B: SMEM_G)
   static constexpr size_t SMEM =
       sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ + (ZC ? 5 * FZ : 0)) + 64 +
       ((NS * IR + 15) / 16) * 16;
+  // gather-mode instantiations also hold the per-row sources (kept out of
+  // the plain kernels: 576 more bytes pushed the telescoped stage 2's 3 CTAs
+  // past the 196 KB carveout, and its L1 from 60 to 28 KB -- 1.04 -> 1.13 ms)
+  static constexpr size_t SMEM_G = SMEM + 3 * IR * 16;
   // CTAs per SM we aim for: shared memory bound (228 KB per SM, 1 KB of it
   // reserved per CTA), at most 8
 #ifndef ORCHA_SMEM_PER_SM
@@ -328,6 +333,16 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   double* Zc = Fz + 2 * 5 * Gm::FZ;                      // [5][H][W] z-face carry (Gm::ZC)
   uint64_t* bar = reinterpret_cast<uint64_t*>(Zc + (Gm::ZC ? 5 * Gm::FZ : 0));
   unsigned char* flipm = reinterpret_cast<unsigned char*>(bar + 8);  // [NS][IR]
+  // gather mode: where staged row r of a plane of z class c (z < 0, inside,
+  // >= NB) comes from -- resolved once per CTA (RowSrc; the per-plane issue
+  // only adds the plane offset)
+  struct RowSrc {
+    const double* base;  // source row (plane 0 of its cube)
+    int zm;              // z image mode of the source entry; -1: the own padded plane
+    short fl;            // sign-flip bits (rho*v: 4, rho*w: 8)
+    short run;           // rows copied from here (0: not the first row of a run)
+  };
+  RowSrc* rsrc = reinterpret_cast<RowSrc*>(flipm + ((NS * Gm::IR + 15) / 16) * 16);  // [3][IR]
 
   const int tid = threadIdx.x;
   const int me = HYB ? smap[blockIdx.x / Gm::NSPLIT] : (int)(blockIdx.x / Gm::NSPLIT);
@@ -380,44 +395,23 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   auto issue = [&](int p) {
     if (p < nplanes) {
       const int s = p % NS, lane = tid & 31;
-      if (GATHER) {
-        // Gather mode: only the x-guards were filled.  Each staged row
-        // (padded plane pp, padded row pr) is the (y, z) image of a row of
-        // the block that owns it -- the neighbour table's (0, oy, oz) entry --
-        // whose x-guards are filled: the axis-ordered ghost fill composed on
-        // the fly (x, then y over x-guards, then z over x,y-guards).  Lane r
-        // resolves row r; rows whose sources are consecutive form one copy,
-        // issued by the lane that starts the run.
+      if (GATHER) {  // the rows' sources of the plane's z class (rsrc, resolved in the prologue)
         const int pp = p + porg, z = pp - INO;
         const int oz = z < 0 ? -1 : (z >= NB ? 1 : 0);
-        const double* rp = nullptr;
-        int fl = 0;
-        if (lane < Gm::IR) {
-          const int pr = jj0 + ORG + lane, y = pr - INO;
-          const int oy = y < 0 ? -1 : (y >= NB ? 1 : 0);
-          const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
-          if (e.src == nullptr) {  // remote source: its rows were exchanged into our own guards
-            rp = in + (long long)pp * Gm::PLANE + (long long)pr * IPX;
-          } else {
-            const int ys = guard_image<NB>(y, oy, (e.mode >> 2) & 3), zs = guard_image<NB>(z, oz, (e.mode >> 4) & 3);
-            rp = e.src + (long long)(zs + INO) * Gm::PLANE + (long long)(ys + INO) * IPX;
-            fl = e.flip & 0xC;  // mirrored y -> negate rho*v (bit 2), z -> rho*w (bit 3)
-          }
-          flipm[s * Gm::IR + lane] = (unsigned char)fl;
-        }
-        const double* prev = (const double*)__shfl_up_sync(0xffffffffu, (unsigned long long)rp, 1);
-        const int pfl = __shfl_up_sync(0xffffffffu, fl, 1);
-        const bool start = lane < Gm::IR && (lane == 0 || rp != prev + IPX || fl != pfl);
-        const unsigned starts = __ballot_sync(0xffffffffu, start);
         if (lane == 0) mbar_expect_tx(&bar[s], 5u * BAND * 8u);
         __syncwarp();
-        if (start) {
-          const unsigned later = starts & ~((2u << lane) - 1u);
-          const int run = (later ? __ffs(later) - 1 : Gm::IR) - lane;
-          fence_proxy_async();
+        if (lane < Gm::IR) {
+          const RowSrc e = rsrc[(oz + 1) * Gm::IR + lane];
+          flipm[s * Gm::IR + lane] = (unsigned char)e.fl;
+          if (e.run) {
+            const int zp = e.zm < 0 ? pp : guard_image<NB>(z, oz, e.zm) + INO;
+            const double* rp = e.base + zp * Gm::PLANE;
+            fence_proxy_async();
 #pragma unroll
-          for (int v = 0; v < 5; v++)
-            bulk_load(ring + (s * 5 + v) * BAND + lane * IPX, rp + v * in_cube, (uint32_t)(run * IPX * 8), &bar[s]);
+            for (int v = 0; v < 5; v++)
+              bulk_load(ring + (s * 5 + v) * BAND + lane * IPX, rp + v * in_cube, (uint32_t)(e.run * IPX * 8),
+                        &bar[s]);
+          }
         }
       } else if (lane == 0) {
         fence_proxy_async();
@@ -597,6 +591,46 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
 
   // ---- prologue: planes 0..4 (z in [K0-2, K0+3)), z-faces K0-1/2 -> Fz[1]
   const bool issuer = ORCHA_ISSUE_LAST ? warp == Gm::NW - 1 : warp == 0;  // the warp that stages planes
+  if (GATHER && issuer) {
+    // Gather mode: only the x-guards were filled.  Each staged row (padded
+    // row pr of padded plane pp) is the (y, z) image of a row of the block
+    // that owns it -- the neighbour table's (0, oy, oz) entry -- whose
+    // x-guards are filled: the axis-ordered ghost fill composed on the fly (x,
+    // then y over x-guards, then z over x,y-guards).  Lane r resolves row r
+    // for each z class (its representative plane: the source entry, and so
+    // which rows are consecutive in memory, is the same for every plane of
+    // the class); rows whose sources are consecutive form one copy, issued by
+    // the lane that starts the run.
+#pragma unroll 1
+    for (int c = 0; c < 3; c++) {
+      const int oz = c - 1, z = oz < 0 ? -1 : oz > 0 ? NB : 0, pp = z + INO;
+      const double* rp = nullptr;
+      RowSrc r{nullptr, -1, 0, 0};
+      if (lane < Gm::IR) {
+        const int pr = jj0 + ORG + lane, y = pr - INO;
+        const int oy = y < 0 ? -1 : (y >= NB ? 1 : 0);
+        const NbrEntry e = snb[(oz + 1) * 3 + (oy + 1)];
+        if (e.src == nullptr) {  // remote source: its rows were exchanged into our own guards
+          r.base = in + (long long)pr * IPX;
+          rp = r.base + (long long)pp * Gm::PLANE;
+        } else {
+          const int ys = guard_image<NB>(y, oy, (e.mode >> 2) & 3);
+          r.zm = (e.mode >> 4) & 3;
+          r.base = e.src + (long long)(ys + INO) * IPX;
+          rp = r.base + (long long)(guard_image<NB>(z, oz, r.zm) + INO) * Gm::PLANE;
+          r.fl = (short)(e.flip & 0xC);  // mirrored y -> negate rho*v (bit 2), z -> rho*w (bit 3)
+        }
+      }
+      const double* prev = (const double*)__shfl_up_sync(0xffffffffu, (unsigned long long)rp, 1);
+      const int pfl = __shfl_up_sync(0xffffffffu, (int)r.fl, 1);
+      const bool start = lane < Gm::IR && (lane == 0 || rp != prev + IPX || r.fl != pfl);
+      const unsigned starts = __ballot_sync(0xffffffffu, start);
+      const unsigned later = starts & ~((2u << lane) - 1u);
+      r.run = start ? (short)((later ? __ffs(later) - 1 : Gm::IR) - lane) : (short)0;
+      if (lane < Gm::IR) rsrc[c * Gm::IR + lane] = r;
+    }
+    __syncwarp();
+  }
   if (issuer)
     for (int p = 0; p < NS; p++) issue(p);
   if (GATHER) __syncthreads();  // the sign-flip masks thread 0 just wrote
@@ -780,7 +814,7 @@ static cudaError_t stage_attrs() {
   constexpr bool P2 = (STAGE == 2) || (MODE == 1);
   constexpr bool GA = (STAGE == 1) || (MODE == 1);
   static cudaError_t once = [] {
-    const int sm = (int)Gm::SMEM;
+    const int sm = (int)Gm::SMEM_G;  // the largest of the instantiations'
     cudaError_t e = cudaFuncSetAttribute(stage_fused_kernel<NB, STAGE, SPLIT, MODE, 0, false, SCH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e == cudaSuccess)
@@ -820,7 +854,7 @@ static void launch_stage(const DevGrid& G, double* state, double* u1, int nslots
   // instantiations so the default kernels carry none of their registers
   const dim3 grid(nslots * SPLIT);
 #define ORCHA_K(P, GT)                                                                                  \
-  stage_fused_kernel<NB, STAGE, SPLIT, MODE, P, GT, SCH><<<grid, Gm::NT, Gm::SMEM, s>>>(G, state, u1, slots, \
+  stage_fused_kernel<NB, STAGE, SPLIT, MODE, P, GT, SCH><<<grid, Gm::NT, GT ? Gm::SMEM_G : Gm::SMEM, s>>>(G, state, u1, slots, \
                                                                                       d_dt, h_dt, records, st, \
                                                                                       push, nbr, nullptr)
   if (push && pushkind == 2) {
@@ -948,10 +982,10 @@ static cudaError_t hybrid_attrs() {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
   static cudaError_t once = [] {
     cudaError_t e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 0>::SMEM);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 0>::SMEM_G);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM);
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM_G);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 2, S, 0>::SMEM);
@@ -983,12 +1017,12 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
     }
     if (nbnd > 0) {
       stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>
-          <<<nbnd * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM, fork ? side : s>>>(
+          <<<nbnd * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM_G, fork ? side : s>>>(
               G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap);
       count_launch();
     }
     if (nint > 0) {
-      stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM, s>>>(
+      stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM_G, s>>>(
           G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap + nbnd);
       count_launch();
     }

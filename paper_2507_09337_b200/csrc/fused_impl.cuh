@@ -108,6 +108,18 @@
 #ifndef ORCHA_XSHFL
 #define ORCHA_XSHFL 0
 #endif
+// z fluxes in registers (ORCHA_ZREG): the z-face task of column w runs in
+// thread w -- the thread that updates cell w of the plane -- so the flux of
+// face k-1/2 stays in its registers for the next plane (and, with the z-face
+// carry, the carried face state too): no Fz double buffer, no Zc slots, no
+// shared stores / loads of z fluxes; the z slots are the last round of the
+// update warps.  Bit 0: stage-1 kernels, bit 1: stage-2 kernels (16^3
+// blocks).  The fluxes and carried state hold 20 registers across the plane
+// loop, so the stage-1 kernels (80 registers at their 3 / 2 CTAs per SM)
+// would spill: stage 2 only by default
+#ifndef ORCHA_ZREG
+#define ORCHA_ZREG 2
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 // 4-deep staging ring for the kernels with the z-face carry (its z-faces
 // never read the plane below the output plane after the prologue)
@@ -203,10 +215,14 @@ struct Geo {
                                              (STAGE == 2 ? ORCHA_EXTRA_WARPS8_2 : ORCHA_EXTRA_WARPS8_1);
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
+  // z slots in the last round of warps 0 .. SZ-1 (the update warps): the x / y
+  // slots must fit the remaining rounds
+  static constexpr bool ZREG = ((ORCHA_ZREG >> (STAGE - 1)) & 1) && NB == 16 && !ORCHA_ONEBAR && !ORCHA_XSHFL &&
+                               SZ <= NW && SZ * (ROUNDS - 1) + (NW - SZ) * ROUNDS >= SX + SY;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
   // (+ the gather mode's per-row sources of the three z classes, 3 x IR x 16 B: SMEM_G)
   static constexpr size_t SMEM =
-      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + 2 * 5 * FZ + (ZC ? 5 * FZ : 0)) + 64 +
+      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + (ZREG ? 0 : 2 * 5 * FZ + (ZC ? 5 * FZ : 0))) + 64 +
       ((NS * IR + 15) / 16) * 16;
   // gather-mode instantiations also hold the per-row sources (kept out of
   // the plain kernels: 576 more bytes pushed the telescoped stage 2's 3 CTAs
@@ -218,7 +234,7 @@ struct Geo {
 #define ORCHA_SMEM_PER_SM 226000
 #endif
   static constexpr int MINB_S = (int)(ORCHA_SMEM_PER_SM / (SMEM + 1024));
-  static constexpr int MINB_R = 65536 / (NT * 80);  // at ~80 registers per thread
+  static constexpr int MINB_R = 65536 / (NT * (ZREG ? 120 : 80));  // at ~80 registers per thread (~120 with ZREG)
   static constexpr int MINB_SR = MINB_S < MINB_R ? MINB_S : MINB_R;
   static constexpr int MINB = MINB_SR < 1 ? 1 : (MINB_SR > 8 ? 8 : MINB_SR);
   static_assert(NT >= FZ, "one update cell per thread");
@@ -329,9 +345,12 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   double* ring = smem;                                   // [NS][5][IR][IPX]
   double* Fx = ring + NS * 5 * BAND;                     // [5][H][W+1]
   double* Fy = Fx + 5 * Gm::FX;                          // [5][H+1][W]
-  double* Fz = Fy + 5 * Gm::FY;                          // [2][5][H][W]
-  double* Zc = Fz + 2 * 5 * Gm::FZ;                      // [5][H][W] z-face carry (Gm::ZC)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Zc + (Gm::ZC ? 5 * Gm::FZ : 0));
+  double* Fz = Fy + 5 * Gm::FY;                          // [2][5][H][W] (not with Gm::ZREG)
+  double* Zc = Fz + (Gm::ZREG ? 0 : 2 * 5 * Gm::FZ);     // [5][H][W] z-face carry (Gm::ZC, not Gm::ZREG)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Zc + (Gm::ZC && !Gm::ZREG ? 5 * Gm::FZ : 0));
+  // Gm::ZREG: this thread's z-face fluxes (k-1/2 and k+1/2) and carried face state
+  double zf_prev[5], zf_cur[5];
+  Prim zcar;
   unsigned char* flipm = reinterpret_cast<unsigned char*>(bar + 8);  // [NS][IR]
   // gather mode: where staged row r of a plane of z class c (z < 0, inside,
   // >= NB) comes from -- resolved once per CTA (RowSrc; the per-plane issue
@@ -523,7 +542,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       // left state of cell k: carried from the previous plane (the prologue
       // face seeds it); cells k, k+1, k+2 give cell k+1's two face states
       Prim L, R, Up, q0, q1, q2;
-      if (it >= 0) {
+      if (it >= 0 && Gm::ZREG) {
+        L = zcar;
+      } else if (it >= 0) {
         L.r = Zc[w];
         L.u = Zc[Gm::FZ + w];
         L.v = Zc[2 * Gm::FZ + w];
@@ -540,19 +561,25 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       ld(ring + ((it + 3) % NS) * 5 * BAND, base, q1);
       ld(ring + ((it + 4) % NS) * 5 * BAND, base, q2);
       plm_cell<SCH>(q0, q1, q2, G, &Up, &R);
-      Zc[w] = Up.r;
-      Zc[Gm::FZ + w] = Up.u;
-      Zc[2 * Gm::FZ + w] = Up.v;
-      Zc[3 * Gm::FZ + w] = Up.w;
-      Zc[4 * Gm::FZ + w] = Up.p;
-      riemann_store<2, SCH>(L, R, G, fz_out + w, Gm::FZ);
+      if constexpr (Gm::ZREG) {
+        zcar = Up;
+        riemann_store<2, SCH>(L, R, G, fz_out, 1);
+      } else {
+        Zc[w] = Up.r;
+        Zc[Gm::FZ + w] = Up.u;
+        Zc[2 * Gm::FZ + w] = Up.v;
+        Zc[3 * Gm::FZ + w] = Up.w;
+        Zc[4 * Gm::FZ + w] = Up.p;
+        riemann_store<2, SCH>(L, R, G, fz_out + w, Gm::FZ);
+      }
     } else {
       Prim q0, q1, q2, q3;
       ld(ring + ((it + 1) % NS) * 5 * BAND, base, q0);
       ld(ring + ((it + 2) % NS) * 5 * BAND, base, q1);
       ld(ring + ((it + 3) % NS) * 5 * BAND, base, q2);
       ld(ring + ((it + 4) % NS) * 5 * BAND, base, q3);
-      face_flux<2, SCH>(q0, q1, q2, q3, G, fz_out + w, Gm::FZ);
+      if constexpr (Gm::ZREG) face_flux<2, SCH>(q0, q1, q2, q3, G, fz_out, 1);
+      else face_flux<2, SCH>(q0, q1, q2, q3, G, fz_out + w, Gm::FZ);
     }
   };
   const int warp = tid >> 5, lane = tid & 31;
@@ -561,10 +588,17 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   int tkind[Gm::ROUNDS], ttask[Gm::ROUNDS], tbase[Gm::ROUNDS];
 #pragma unroll
   for (int r = 0; r < Gm::ROUNDS; r++) {
-    const int m = r * Gm::NW + warp;
+    // Gm::ZREG: z slot w in the last round of warp w (w < SZ); the x / y
+    // slots, in order, over the remaining (round, warp) positions
+    const bool zslot = Gm::ZREG && warp < Gm::SZ && r == Gm::ROUNDS - 1;
+    const int m = !Gm::ZREG ? r * Gm::NW + warp
+                  : zslot ? Gm::SX + Gm::SY + warp
+                  : r < Gm::ROUNDS - 1 ? r * Gm::NW + warp
+                  : (Gm::ROUNDS - 1) * Gm::NW + warp - Gm::SZ;
+    const int mm = (Gm::ZREG && !zslot && m >= Gm::SX + Gm::SY) ? Gm::NSLOT : m;  // x / y positions left over
     int kind = 3, t = 0;
     int xbase = 0;
-    if (m < Gm::SX) {
+    if (mm < Gm::SX) {
       if constexpr (ORCHA_XSHFL) {
         // cell c of the band plane's rows of W+2 x-slope cells (output
         // columns -1 .. W); every lane of the slot runs the task (shuffle)
@@ -578,8 +612,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         kind = t < Gm::FX ? 0 : 3;
       }
     }
-    else if (m < Gm::SX + Gm::SY) { t = (m - Gm::SX) * 32 + lane; kind = t < Gm::FY ? 1 : 3; }
-    else if (m < Gm::NSLOT) { t = (m - Gm::SX - Gm::SY) * 32 + lane; kind = t < Gm::FZ ? 2 : 3; }
+    else if (mm < Gm::SX + Gm::SY) { t = (mm - Gm::SX) * 32 + lane; kind = t < Gm::FY ? 1 : 3; }
+    else if (mm < Gm::NSLOT) { t = (mm - Gm::SX - Gm::SY) * 32 + lane; kind = t < Gm::FZ ? 2 : 3; }
     tkind[r] = kind;
     ttask[r] = t;
     tbase[r] = (ORCHA_XSHFL && kind == 0) ? xbase : kind < 3 ? task_base(kind, t) : 0;
@@ -639,7 +673,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     convert(p);
   }
   __syncthreads();
-  for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
+  if constexpr (Gm::ZREG) {
+    if (tid < Gm::FZ) z_task(tid, task_base(2, tid), -1, zf_prev);
+  } else {
+    for (int w = tid; w < Gm::FZ; w += NT) z_task(w, task_base(2, w), -1, Fz + 5 * Gm::FZ);
+  }
   __syncthreads();
   if (issuer)  // into the slots of planes 0 (and 1: a 4-deep ring, dead once the prologue faces are done)
     for (int p = NS; p < 6; p++) issue(p);
@@ -697,7 +735,8 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
       else if (tkind[r] == 1) y_task(ttask[r], tbase[r], it);
       else if (tkind[r] == 2) {
         if (ORCHA_ONEBAR == 2 && it > 0) mbar_wait(cdone, (it - 1) & 1);  // plane it+4 converted
-        z_task(ttask[r], tbase[r], it, fz_cur);
+        if constexpr (Gm::ZREG) z_task(ttask[r], tbase[r], it, zf_cur);
+        else z_task(ttask[r], tbase[r], it, fz_cur);
       }
     }
     constexpr int UW = UWARPS;
@@ -734,8 +773,13 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         for (int v = 0; v < 5; v++) {
           double tx = (Fx[v * Gm::FX + lj * (W + 1) + li + 1] - Fx[v * Gm::FX + lj * (W + 1) + li]) * G.id[0];
           double ty = (Fy[v * Gm::FY + (lj + 1) * W + li] - Fy[v * Gm::FY + lj * W + li]) * G.id[1];
-          double tz = (fz_cur[v * Gm::FZ + tid] - fz_prev[v * Gm::FZ + tid]) * G.id[2];
+          double tz = Gm::ZREG ? (zf_cur[v] - zf_prev[v]) * G.id[2]
+                               : (fz_cur[v * Gm::FZ + tid] - fz_prev[v * Gm::FZ + tid]) * G.id[2];
           D[v] = (tx + ty) + tz;
+        }
+        if constexpr (Gm::ZREG) {  // face k+1/2 is the next plane's k-1/2
+#pragma unroll
+          for (int v = 0; v < 5; v++) zf_prev[v] = zf_cur[v];
         }
       }
       if (ORCHA_ONEBAR) {  // the face arrays of plane it are consumed: the faces of it+1 may overwrite them

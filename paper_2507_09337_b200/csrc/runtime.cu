@@ -858,6 +858,8 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
   return fill_impl_body(pk, npk, comm, buffer, faces_only, stream, only);
 }
 
+static cudaError_t hyb_side(orcha_packet* p);
+
 static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer,
                               bool faces_only, void* stream, int only) {
   if (!pk || npk < 1) return fail(ORCHA_E_ARG, "no packets");
@@ -964,6 +966,10 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
   }
   for (int q = 0; q < npk; q++) {
     if (only >= 0 && q != only) continue;
+    if (f->d_hyb_smap && q == 0) {  // the borrowed ring's side stream, ahead of the advance
+      cudaError_t e = hyb_side(pk[q]);
+      if (e != cudaSuccess) return cuda_fail(e, "side stream");
+    }
     pk[q]->d_push = f->d_push[q];
     pk[q]->d_push_u1 = f->d_push_u1[q];
     pk[q]->push_plan = f;

@@ -92,8 +92,9 @@ def borrowed_ring_regions(brick, nb=16):
     """Stage-1 output region of each block of a rank's brick under the
     borrowed ring (include/orcha.h orcha_set_ring_mode): self sides are the
     brick faces (a physical boundary or another rank); blocks with an x or y
-    self side run the box kernel (20 x 20 columns), the rest the interior
-    kernel; both extend the planes by 2 on each self z side."""
+    self side run the box kernel (20 x 20 columns; 18 x 18 for 16^3 blocks
+    with at most one self side per axis), the rest the interior kernel; all
+    extend the planes by 2 on each self z side."""
     out = []
     for k in range(brick[2]):
         for j in range(brick[1]):
@@ -101,7 +102,12 @@ def borrowed_ring_regions(brick, nb=16):
                 sx = (i == 0) + (i == brick[0] - 1)
                 sy = (j == 0) + (j == brick[1] - 1)
                 sz = (k == 0) + (k == brick[2] - 1)
-                w = nb + 4 if (sx or sy) else nb
+                if not (sx or sy):
+                    w = nb
+                elif nb == 16 and sx < 2 and sy < 2:
+                    w = nb + 2
+                else:
+                    w = nb + 4
                 out.append((w, w, nb + 2 * sz))
     return out
 

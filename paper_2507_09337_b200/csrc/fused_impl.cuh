@@ -170,19 +170,25 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // scratch, no refill); MODE 1 = per-stage step (both stages
 // on the interior, U1 in a padded (n+8)^3 scratch whose guards are refilled
 // between the stages).
-template <int NB, int STAGE, int SPLIT, int MODE = 0>
+// WXT / HT (borrowed-ring stage 1 of blocks with one x and/or one y self
+// side): output columns and band rows other than the square default; the x /
+// y output origin is then chosen per CTA (the self side's 2 ring columns /
+// rows).
+template <int NB, int STAGE, int SPLIT, int MODE = 0, int WXT = 0, int HT = 0>
 struct Geo {
-  static constexpr int W = (STAGE == 1 && MODE == 0) ? NB + 4 : NB;  // output columns (and rows) per plane
-  static constexpr int OFF = (W - NB) / 2;                   // output origin (interior-relative) = -OFF
+  static constexpr int W0 = (STAGE == 1 && MODE == 0) ? NB + 4 : NB;  // default output columns, rows, planes
+  static constexpr int W = WXT ? WXT : W0;                   // output columns per plane
+  static constexpr int OFF = (W0 - NB) / 2;                  // default output origin (interior-relative) = -OFF
   static constexpr int K0 = -OFF;                            // first output plane
-  static constexpr int NK = W;                               // output planes
+  static constexpr int NK = W0;                              // output planes
   static constexpr int INO = (STAGE == 1 || MODE == 1) ? 4 : 2;  // input origin offset (guards / ring)
   static constexpr int ORG = INO - 2 - OFF;                  // first staged padded row / plane
   static constexpr int IPX = NB + 2 * INO;                   // padded input row length (= plane rows)
   static constexpr int PLANE = IPX * IPX;                    // doubles per input plane per variable
   static constexpr int NPLANES = NK + 4;                     // input planes streamed
   static constexpr int NSPLIT = SPLIT;                       // row bands per block
-  static constexpr int H = W / NSPLIT;                       // output rows per CTA
+  static constexpr int H = HT ? HT : W0 / NSPLIT;           // output rows per CTA
+  static constexpr int WY = H * NSPLIT;                      // output rows per plane
   static constexpr int IR = H + 4;                           // staged input rows per plane
   static constexpr int BAND = IR * IPX;                      // doubles per staged band per variable
   // z-face carry (see ORCHA_ZCARRY): bit 0 stage 1 of both methods, bit 1 the
@@ -211,7 +217,7 @@ struct Geo {
                             : MODE == 1 ? ORCHA_EXTRA_WARPS_PS
                                         : (STAGE == 1 ? ORCHA_EXTRA_WARPS1 : ORCHA_EXTRA_WARPS2);
   static constexpr int NW = (NB >= 16) ? (NSLOT + RQ - 1) / RQ + XW
-                                       : (ORCHA_ROUNDS8 > 0 ? (NW8 > NWU ? NW8 : NWU) : (W * W + 31) / 32) +
+                                       : (ORCHA_ROUNDS8 > 0 ? (NW8 > NWU ? NW8 : NWU) : (W * H + 31) / 32) +
                                              (STAGE == 2 ? ORCHA_EXTRA_WARPS8_2 : ORCHA_EXTRA_WARPS8_1);
   static constexpr int NT = NW * 32;
   static constexpr int ROUNDS = (NSLOT + NW - 1) / NW;
@@ -325,15 +331,16 @@ __device__ __forceinline__ void push_u1(const PushEntry* sxp, int U1C, int ci, i
 // launch_hybrid_nb): U1 always in the compact (n+4)^3 cubes, the CTA's slot
 // and its self-ring sides from smap (slot | mask << 26), ring cells written
 // only on self sides, the x-ring of the x-neighbours pushed (push_x_u1).
-template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER, int SCH, int HYB = 0>
-__global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE, SPLIT, MODE>::MINB)
+template <int NB, int STAGE, int SPLIT, int MODE, int PUSH, bool GATHER, int SCH, int HYB = 0, int WXT = 0,
+          int HT = 0>
+__global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::MINB)
     stage_fused_kernel(DevGrid G, double* __restrict__ state, double* __restrict__ u1,
                        const SlotInfo* __restrict__ slots, const double* __restrict__ d_dt, double h_dt,
                        DtRecord* __restrict__ rec, DevStatus* st, const PushEntry* __restrict__ push,
                        const NbrEntry* __restrict__ nbr, const int* __restrict__ smap) {
-  using Gm = Geo<NB, STAGE, SPLIT, MODE>;
-  constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS, OFF = Gm::OFF;
-  constexpr int NT = Gm::NT, H = Gm::H, ORG = Gm::ORG;
+  using Gm = Geo<NB, STAGE, SPLIT, MODE, WXT, HT>;
+  constexpr int W = Gm::W, IPX = Gm::IPX, BAND = Gm::BAND, INO = Gm::INO, NS = Gm::NS;
+  constexpr int NT = Gm::NT, H = Gm::H;
   // U1 cube stride: (n+4)^3 compact scratch (telescoped, and every hybrid
   // kernel) or the padded state layout (per-stage)
   constexpr bool CU1 = MODE == 0 || HYB;
@@ -374,6 +381,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   const int zhi = (HYB && STAGE == 1) ? ((selfm >> 5) & 1) * 2 : Gm::OFF;
   const int kz0 = -zlo, nk = NB + zlo + zhi, nplanes = nk + 4;
   const int porg = INO - 2 - zlo;  // padded plane of staged plane 0
+  // output columns [-ox, W - ox), rows [-oy, WY - oy): centred, or (one ring
+  // side wider than the interior) on the self side
+  const int ox = (W - NB == 2) ? ((selfm & 1) ? 2 : (selfm & 2) ? 0 : 1) : (W - NB) / 2;
+  const int oy = (Gm::WY - NB == 2) ? ((selfm & 4) ? 2 : (selfm & 8) ? 0 : 1) : (Gm::WY - NB) / 2;
+  const int ORG = INO - 2 - oy;  // padded row of staged row 0 of band 0
   const int jj0 = band * H;                              // first output row of the band (0-based)
   constexpr int cube = cube_c<NB>();  // == G.cube (checked at launch)
   const double dt = d_dt ? *d_dt : h_dt;
@@ -492,14 +504,14 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
   auto task_base = [&](int kind, int t) -> int {
     if (kind == 0) {
       int j = t / (W + 1), f = t - j * (W + 1);
-      return (j + 2) * IPX + (f - OFF - 2 + INO);
+      return (j + 2) * IPX + (f - ox - 2 + INO);
     }
     if (kind == 1) {
       int f = t / W, i = t - f * W;
-      return f * IPX + (i - OFF + INO);
+      return f * IPX + (i - ox + INO);
     }
     int j = t / W, i = t - j * W;
-    return (j + 2) * IPX + (i - OFF + INO);
+    return (j + 2) * IPX + (i - ox + INO);
   };
   auto x_task = [&](int t, int base, int it) {
     const double* P = ring + ((it + 2) % NS) * 5 * BAND;
@@ -606,7 +618,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
         const int j = cc / (W + 2), u = cc - j * (W + 2);
         kind = 0;
         t = (c < Gm::NCX && lane < 31 && u <= W) ? j * (W + 1) + u : -1;
-        xbase = (j + 2) * IPX + (u - 2 - OFF + INO);
+        xbase = (j + 2) * IPX + (u - 2 - ox + INO);
       } else {
         t = m * 32 + lane;
         kind = t < Gm::FX ? 0 : 3;
@@ -696,7 +708,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE>::NT, Geo<NB, STAGE
     // prefetch the update operands of this thread's cell of plane k
     const bool upd = tid < Gm::FZ;
     const int lj = upd ? tid / W : 0, li = upd ? tid - (tid / W) * W : 0;
-    const int ci = li - OFF, cj = jj0 + lj - OFF;
+    const int ci = li - ox, cj = jj0 + lj - oy;
     const int so = coff<NB>(ci, cj, k);
     double un[5], v1[5];
     if (upd) {
@@ -1011,7 +1023,10 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
 // owns) or an owner on another rank (no second exchange) -- need the ring
 // computed.  So stage 1 runs in two launches over the slot map:
 //   smap[0, nbnd):        blocks with an x or y self side: the box kernel
-//                         (MODE 0 geometry: 20 x 20 output columns of 16^3);
+//                         (MODE 0 geometry: 20 x 20 output columns of 16^3),
+//                         or for 16^3 blocks with at most one self side per
+//                         axis the 18 x 18 kernel (the ring columns / rows of
+//                         the self side; nb4 counts the groups);
 //   smap[nbnd, +nint):    the rest: the interior kernel (MODE 1 geometry);
 // in both the output planes are the interior plus the 2 ring planes on the
 // self z sides only (runtime plane range), and ring cells are stored on
@@ -1033,6 +1048,12 @@ static cudaError_t hybrid_attrs() {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 2, S, 0>::SMEM);
+    if constexpr (NB == 16) {
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1, NB + 2, (NB + 2) / S>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>::SMEM_G);
+    }
     return e;
   }();
   return once;
@@ -1040,7 +1061,7 @@ static cudaError_t hybrid_attrs() {
 
 template <int NB, int SCH>
 static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
-                                    const int* smap, int nbnd, int nint, const PushEntry* hpush,
+                                    const int* smap, const int* nb4, int nint, const PushEntry* hpush,
                                     const NbrEntry* nbr, const double* d_dt, double h_dt,
                                     DtRecord* records, long long* nrecords, DevStatus* st, cudaStream_t s,
                                     const PushEntry* push, int parts, cudaStream_t side, cudaEvent_t ev_fork,
@@ -1051,23 +1072,41 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
   if (e != cudaSuccess) return e;
   if (parts & 1) {
     PhaseScope ph(PH_STAGE1, s);
-    // side stream (optional): the box kernel runs beside the interior one
-    // (they read only U^n and write disjoint cells), filling each other's tail
+    // side stream (optional): the blocks with x / y self sides run beside the
+    // interior kernel (they read only U^n and write disjoint cells), filling
+    // each other's tail
+    const int nbnd = nb4[0] + nb4[1] + nb4[2] + nb4[3];
     const bool fork = side != nullptr && nbnd > 0 && nint > 0;
     if (fork) {
       e = cudaEventRecord(ev_fork, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_fork, 0);
       if (e != cudaSuccess) return e;
     }
-    if (nbnd > 0) {
+    cudaStream_t sb = fork ? side : s;
+    const int* sm = smap;
+    // the box (two x or two y self sides: a one-block-wide brick; every NB)
+    if (nb4[0] > 0) {
       stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>
-          <<<nbnd * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM_G, fork ? side : s>>>(
-              G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap);
+          <<<nb4[0] * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt,
+                                                                              records, st, hpush, nbr, sm);
       count_launch();
+    }
+    sm += nb4[0];
+    if constexpr (NB == 16) {
+      // at most one self side per axis: 18 x 18 output columns / rows, the
+      // 2 ring columns (rows) on the self side, or one on each side of an
+      // axis without one (computed, not stored)
+      if (nb4[1] > 0) {
+        using GC = Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>;
+        stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1, NB + 2, (NB + 2) / S>
+            <<<nb4[1] * S, GC::NT, GC::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
+        count_launch();
+      }
+      sm += nb4[1];
     }
     if (nint > 0) {
       stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM_G, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, smap + nbnd);
+          G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
       count_launch();
     }
     if (fork) {
@@ -1120,13 +1159,13 @@ static cudaError_t preload_nb() {
     return e == cudaSuccess ? hybrid_attrs<NB, SCH>() : e;                                                       \
   }                                                                                                              \
   cudaError_t fused_hybrid_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,              \
-                                          const SlotInfo* slots, const int* smap, int nbnd, int nint,            \
+                                          const SlotInfo* slots, const int* smap, const int* nb4, int nint,            \
                                           const PushEntry* hpush, const NbrEntry* nbr,                           \
                                           const double* d_dt, double h_dt, DtRecord* records,                    \
                                           long long* nrecords, DevStatus* st, cudaStream_t s,                    \
                                           const PushEntry* push, int parts, cudaStream_t side,                   \
                                           cudaEvent_t ev_fork, cudaEvent_t ev_join) {                            \
-    return launch_hybrid_nb<NB, SCH>(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, d_dt, h_dt,       \
+    return launch_hybrid_nb<NB, SCH>(G, state, u1, nslots, slots, smap, nb4, nint, hpush, nbr, d_dt, h_dt,       \
                                      records, nrecords, st, s, push, parts, side, ev_fork, ev_join);              \
   }
 

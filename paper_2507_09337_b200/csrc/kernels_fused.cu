@@ -16,7 +16,7 @@ namespace orcha {
                                          cudaStream_t s, const PushEntry* push, const NbrEntry* nbr, int pk); \
   cudaError_t fused_preload_n##NB##_s##SCH();                                                                   \
   cudaError_t fused_hybrid_n##NB##_s##SCH(const DevGrid& G, double* state, double* u1, int nslots,              \
-                                          const SlotInfo* slots, const int* smap, int nbnd, int nint,            \
+                                          const SlotInfo* slots, const int* smap, const int* nb4, int nint,            \
                                           const PushEntry* hpush, const NbrEntry* nbr,                           \
                                           const double* d_dt, double h_dt, DtRecord* records,                    \
                                           long long* nrecords, DevStatus* st, cudaStream_t s,                    \
@@ -78,13 +78,13 @@ cudaError_t launch_advance_fused(const DevGrid& G, double* state, double* u1, in
 // same result as the telescoped step with the stage-1 ring computed only on
 // the self sides smap names.  Fused 3D shapes only (fused_supported).
 cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
-                                  const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
+                                  const int* smap, const int* nb4, int nint, const PushEntry* hpush, const NbrEntry* nbr,
                                   const double* d_dt, double h_dt, DtRecord* records,
                                   long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                   int parts, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join) {
   const bool var = G.riemann != 0 || G.limiter != 0 || G.eos != 0;
 #define ORCHA_HYB(NB, SCH)                                                                                  \
-  fused_hybrid_n##NB##_s##SCH(G, state, u1, nslots, slots, smap, nbnd, nint, hpush, nbr, d_dt, h_dt,       \
+  fused_hybrid_n##NB##_s##SCH(G, state, u1, nslots, slots, smap, nb4, nint, hpush, nbr, d_dt, h_dt,       \
                               records, nrecords, st, s, push, parts, side, ev_fork, ev_join)
   if (G.nb[0] == 16) return var ? ORCHA_HYB(16, 1) : ORCHA_HYB(16, 0);
   if (G.nb[0] == 32) return var ? ORCHA_HYB(32, 1) : ORCHA_HYB(32, 0);

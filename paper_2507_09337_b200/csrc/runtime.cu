@@ -69,7 +69,7 @@ bool fused_supported(const DevGrid& G);
 cudaError_t fused_preload(const DevGrid& G);
 long long fused_u1_cube(int nb);
 cudaError_t launch_advance_hybrid(const DevGrid& G, double* state, double* u1, int nslots, const SlotInfo* slots,
-                                  const int* smap, int nbnd, int nint, const PushEntry* hpush, const NbrEntry* nbr,
+                                  const int* smap, const int* nb4, int nint, const PushEntry* hpush, const NbrEntry* nbr,
                                   const double* d_dt, double h_dt, DtRecord* records,
                                   long long* nrecords, DevStatus* st, cudaStream_t s, const PushEntry* push,
                                   int parts, cudaStream_t side, cudaEvent_t ev_fork, cudaEvent_t ev_join);
@@ -251,7 +251,8 @@ struct FillPlan {
   // launch_hybrid_nb): the slot map (slots with a self side first, each entry
   // slot | self-side mask << 26) and the ring push table (face directions)
   int* d_hyb_smap = nullptr;
-  int hyb_nbnd = 0, hyb_nint = 0;
+  int hyb_nb4[4] = {0, 0, 0, 0};  // box, 18x18 (16^3; other sizes: box only), unused, unused
+  int hyb_nint = 0;
   PushEntry* d_hyb_push = nullptr;
 };
 // Frees a plan's device tables and the plan (not its packets' pointers).
@@ -763,7 +764,7 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     // the block computes its stage-1 ring itself, elsewhere it borrows it
     orcha_packet* p = pk[0];
     const long long U1C = fused_u1_cube(G.nb[0]);
-    std::vector<int> bnd, inr;
+    std::vector<int> grp[4], inr;
     std::vector<PushEntry> hp((size_t)p->nslots * 27, PushEntry{nullptr, 0, 0});
     auto local_slot = [&](const int bc[3], const int o[3], int* mode) -> int {
       HostEntry h = make_entry(g, bc, o);
@@ -787,13 +788,21 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
           else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
                    PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
         }
-      // x / y self sides: the box kernel; none, or z only: the interior
-      // kernel (its plane range extended on the self z sides)
-      ((mask & 15) ? bnd : inr).push_back(s | (mask << 26));
+      // x / y self sides: the box kernel, or (16^3) the 18 x 18 kernel
+      // when at most one side of each axis is self; none, or z only: the
+      // interior kernel (plane ranges extended on self z sides)
+      const int sx = (mask & 1) + ((mask >> 1) & 1), sy = ((mask >> 2) & 1) + ((mask >> 3) & 1);
+      const int e = s | (mask << 26);
+      if (sx == 0 && sy == 0) inr.push_back(e);
+      else if (G.nb[0] != 16 || sx == 2 || sy == 2) grp[0].push_back(e);
+      else grp[1].push_back(e);
     }
-    std::vector<int> smap = bnd;
+    std::vector<int> smap;
+    for (int k = 0; k < 4; k++) {
+      smap.insert(smap.end(), grp[k].begin(), grp[k].end());
+      f->hyb_nb4[k] = (int)grp[k].size();
+    }
     smap.insert(smap.end(), inr.begin(), inr.end());
-    f->hyb_nbnd = (int)bnd.size();
     f->hyb_nint = (int)inr.size();
     cudaError_t err = cudaMalloc(&f->d_hyb_smap, smap.size() * sizeof(int));
     if (err == cudaSuccess)
@@ -1211,7 +1220,7 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   else if (!p->peer_comm && xpush && ring_mode() == 1 && p->push_plan->d_hyb_smap &&
            p->d_nbr == p->push_plan->d_tables[0] && (e = hyb_side(p)) == cudaSuccess)
     e = launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, p->push_plan->d_hyb_smap,
-                              p->push_plan->hyb_nbnd, p->push_plan->hyb_nint, p->push_plan->d_hyb_push, p->d_nbr,
+                              p->push_plan->hyb_nb4, p->push_plan->hyb_nint, p->push_plan->d_hyb_push, p->d_nbr,
                               d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3,
                               hyb_concurrent() ? p->side : nullptr, p->ev_ready, p->ev_halo);
   else if (!p->peer_comm)

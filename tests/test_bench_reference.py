@@ -30,15 +30,17 @@ def test_reference_arm_json_line():
 def test_work_model_reproduces_survey_rows():
     # the fp64 work model reproduces SURVEY 8(d)'s literal
     # telescoped 16^3 step (1498, by construction) and its per-stage row
-    # (1033) to 1 %; the borrowed ring on cfg4's 16^3-block brick is 1100
+    # (1033) to 1 %; the borrowed ring on cfg4's 16^3-block brick is 1065
     sys.path.insert(0, ROOT)
     import bench
     assert abs(bench.step_fp64_model([(20, 20, 20)] * 8) - 1498.0) < 1e-9
     assert abs(bench.step_fp64_model([(16, 16, 16)] * 8) / 1033.0 - 1) < 0.01
     regions = bench.borrowed_ring_regions((16, 16, 16))
     assert len(regions) == 4096
-    assert sum(r[0] == 20 for r in regions) == 16 ** 3 - 16 * 14 * 14          # an x or y brick face
+    assert sum(r[0] == 18 for r in regions) == 16 ** 3 - 16 * 14 * 14          # an x or y brick face
     assert sum(r == (16, 16, 18) for r in regions) == 2 * 14 * 14              # z faces only
-    assert abs(bench.step_fp64_model(regions) - 1100.3) < 0.1
+    assert abs(bench.step_fp64_model(regions) - 1065.3) < 0.1
+    # a brick one block wide in x: both x sides self, the 20 x 20 box
+    assert all(r[0] == 20 for r in bench.borrowed_ring_regions((1, 4, 4)))
     # one block, every side self: the literal box
     assert abs(bench.step_fp64_model(bench.borrowed_ring_regions((1, 1, 1))) - 1498.0) < 1e-9

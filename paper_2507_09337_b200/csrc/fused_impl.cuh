@@ -841,11 +841,17 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
         Prim q = (SCH == 0) ? eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2)
                             : eos_var(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
         double s = (SCH == 0) ? signal_speed<3>(q, G) : signal_speed_var<3>(q, G);
-        long long g = (((long long)si.bc[2] * NB + k) * G.N[1] + ((long long)si.bc[1] * NB + cj)) * G.N[0] +
-                      ((long long)si.bc[0] * NB + ci);
-        if (dt_better(s, g, s_rec, g_rec)) { s_rec = s; g_rec = g; }
+        auto gidx = [&]() -> long long {
+          return (((long long)si.bc[2] * NB + k) * G.N[1] + ((long long)si.bc[1] * NB + cj)) * G.N[0] +
+                 ((long long)si.bc[0] * NB + ci);
+        };
+        // this thread's cells come in increasing k at a fixed (i, j), so their
+        // global indices increase: dt_better(s, g, s_rec, g_rec) reduces to a
+        // larger s, or the first NaN -- g is formed only when the record moves
+        const bool sn = s != s, rn = s_rec != s_rec;
+        if (sn ? !rn : (!rn && s > s_rec)) { s_rec = s; g_rec = gidx(); }
         bool finite = isfinite(nw[0]) && isfinite(nw[1]) && isfinite(nw[2]) && isfinite(nw[3]) && isfinite(nw[4]);
-        if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)g);
+        if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)gidx());
       }
       }
     }

@@ -189,6 +189,10 @@ struct Geo {
   static constexpr int NSPLIT = SPLIT;                       // row bands per block
   static constexpr int H = HT ? HT : W0 / NSPLIT;           // output rows per CTA
   static constexpr int WY = H * NSPLIT;                      // output rows per plane
+  // staged cells converted per band (kernel convert): output rows x output
+  // columns +- 2, then the 4 y-halo rows x output columns
+  static constexpr int NXR = H * (W + 4);
+  static constexpr int NCONV = NXR + 4 * W;
   static constexpr int IR = H + 4;                           // staged input rows per plane
   static constexpr int BAND = IR * IPX;                      // doubles per staged band per variable
   // z-face carry (see ORCHA_ZCARRY): bit 0 stage 1 of both methods, bit 1 the
@@ -285,6 +289,12 @@ __device__ __forceinline__ void push_x(const DevGrid& G, const PushEntry* sxp, i
   if (side < 0 || sxp[side].dst == nullptr) return;
   const PushEntry e = sxp[side];
   const int m = e.mode & 3;
+  if (m == kShift) {  // the neighbour's guard: one plain copy (no sign flip)
+    double* q = e.dst + coff<NB>(side ? ci - NB : ci + NB, cj, k);
+#pragma unroll
+    for (int v = 0; v < 5; v++) q[v * cube_c<NB>()] = w[v];
+    return;
+  }
   int t0, cnt = 1;
   if (m == kShift) t0 = side ? ci - NB : ci + NB;
   else if (m == kMirror) t0 = side ? 2 * NB - 1 - ci : -1 - ci;
@@ -386,6 +396,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
   const int ox = (W - NB == 2) ? ((selfm & 1) ? 2 : (selfm & 2) ? 0 : 1) : (W - NB) / 2;
   const int oy = (Gm::WY - NB == 2) ? ((selfm & 4) ? 2 : (selfm & 8) ? 0 : 1) : (Gm::WY - NB) / 2;
   const int ORG = INO - 2 - oy;  // padded row of staged row 0 of band 0
+  const int ccol0 = INO - ox;    // staged column of output column 0
   const int jj0 = band * H;                              // first output row of the band (0-based)
   constexpr int cube = cube_c<NB>();  // == G.cube (checked at launch)
   const double dt = d_dt ? *d_dt : h_dt;
@@ -409,8 +420,9 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
   // band is small enough), instead of the converting warps taking all of it
   // (3 rounds in both stage-1 kernels against one update).  Measured slower
   // (2.46 vs 2.40 ms per cfg4 step, profiles/r02_ab_convbal.txt): off
-  constexpr int CONV_END = (CSPLIT && ORCHA_CONV_BAL && 2 * (Gm::NW - UWARPS) * 32 < BAND)
-                               ? 2 * (Gm::NW - UWARPS) * 32 : BAND;
+  constexpr int NXR = Gm::NXR, NCONV = Gm::NCONV;
+  constexpr int CONV_END = (CSPLIT && ORCHA_CONV_BAL && 2 * (Gm::NW - UWARPS) * 32 < NCONV)
+                               ? 2 * (Gm::NW - UWARPS) * 32 : NCONV;
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&bar[s], 1);
     mbar_init(fdone, UWARPS);
@@ -457,13 +469,27 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
   };
   auto wait_plane = [&](int p) { mbar_wait(&bar[p % NS], (p / NS) & 1); };
   // EOS in place over the staged band of plane p: cells c0, c0 + nthr, ...
-  auto convert = [&](int p, int c0 = -1, int nthr = Gm::NT, int cend = Gm::BAND) {
+  // Only the staged cells some stencil reads are converted (compact index
+  // c < NCONV): the output rows x (the output columns +- 2: x-faces), then the
+  // 2 + 2 y-halo rows x the output columns (y-faces); the corner cells of the
+  // staged band and its columns beyond +- 2 are never read.
+  auto convert = [&](int p, int c0 = -1, int nthr = Gm::NT, int cend = Gm::NCONV) {
     double* Q = ring + (p % NS) * 5 * BAND;
     const int z = kz0 - 2 + p;
     unsigned long long hits = 0;
-    for (int c = (c0 < 0 ? tid : c0); c < cend; c += nthr) {
+    for (int ci = (c0 < 0 ? tid : c0); ci < cend; ci += nthr) {
       bool fl;
-      int r = c / IPX;
+      int r, col;
+      if (ci < NXR) {
+        r = ci / (W + 4);
+        col = ccol0 - 2 + (ci - r * (W + 4));
+        r += 2;
+      } else {
+        const int c2 = ci - NXR, rr = c2 / W;
+        r = rr < 2 ? rr : H + rr;
+        col = ccol0 + (c2 - rr * W);
+      }
+      const int c = r * IPX + col;
       double my = Q[2 * BAND + c], mz = Q[3 * BAND + c];
       if (GATHER) {  // gather mode: mirrored guard rows negate rho*v / rho*w
         const unsigned fm = flipm[(p % NS) * Gm::IR + r];
@@ -472,7 +498,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
       }
       Prim q = (SCH == 0) ? eos(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl)
                           : eos_var(Q[c], Q[BAND + c], my, mz, Q[4 * BAND + c], G, &fl);
-      int x = c - r * IPX - INO, y = jj0 + ORG + r - INO;
+      int x = col - INO, y = jj0 + ORG + r - INO;
       // own (non-overlapping) rows of the band only, so each cell counts once
       bool mine = r >= 2 && r < 2 + H;
       if (mine && x >= 0 && x < NB && y >= 0 && y < NB && z >= 0 && z < NB) {
@@ -850,15 +876,18 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
         // larger s, or the first NaN -- g is formed only when the record moves
         const bool sn = s != s, rn = s_rec != s_rec;
         if (sn ? !rn : (!rn && s > s_rec)) { s_rec = s; g_rec = gidx(); }
-        bool finite = isfinite(nw[0]) && isfinite(nw[1]) && isfinite(nw[2]) && isfinite(nw[3]) && isfinite(nw[4]);
+        // finite: no exponent field of all ones (integer tests of the high words)
+        bool finite = true;
+#pragma unroll
+        for (int v = 0; v < 5; v++) finite &= (__double2hiint(nw[v]) & 0x7ff00000) != 0x7ff00000;
         if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)gidx());
       }
       }
     }
-    if constexpr (CONV_END < BAND) {  // the update warps' share of the next plane's EOS
+    if constexpr (CONV_END < NCONV) {  // the update warps' share of the next plane's EOS
       if (warp < UWARPS && it + 5 < nplanes) {
         wait_plane(it + 5);
-        convert(it + 5, CONV_END + tid, UWARPS * 32, BAND);
+        convert(it + 5, CONV_END + tid, UWARPS * 32, NCONV);
       }
     }
     if (!ORCHA_ONEBAR) __syncthreads();

@@ -1,5 +1,7 @@
-"""Write profiles/traffic.json: DRAM bytes (read + write) per advance launch
-pair (stage_fused_kernel<16,1> + <16,2>) from an ncu --set full report."""
+"""Write profiles/traffic.json: DRAM bytes (read + write) per advance (every
+stage_fused_kernel<16,1,...> launch of one step -- the borrowed ring's box /
+18 x 18 and interior kernels -- plus <16,2>) from an ncu --set full report
+holding one step's launches."""
 import csv
 import json
 import subprocess
@@ -19,7 +21,7 @@ for row in r[2:]:
         i = h.index(k)
         b += float(row[i]) * scale[units[i]]
     key = "stage1" if "16, 1" in name else "stage2" if "16, 2" in name else name[:40]
-    per.setdefault(key, b)
+    per[key] = per.get(key, 0.0) + b
 tot = per.get("stage1", 0.0) + per.get("stage2", 0.0)
 src = sys.argv[3] if len(sys.argv) > 3 else rep
 json.dump({"advance_bytes_per_launch": tot, "per_kernel_bytes": per, "source": src,

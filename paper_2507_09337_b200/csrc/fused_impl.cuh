@@ -120,6 +120,9 @@
 #ifndef ORCHA_ZREG
 #define ORCHA_ZREG 2
 #endif
+#ifndef ORCHA_STATIC3
+#define ORCHA_STATIC3 0
+#endif
 // ORCHA_ISSUE_LAST=1 (experiment): the last warp issues the staging copies
 // 4-deep staging ring for the kernels with the z-face carry (its z-faces
 // never read the plane below the output plane after the prologue)
@@ -229,6 +232,10 @@ struct Geo {
   // slots must fit the remaining rounds
   static constexpr bool ZREG = ((ORCHA_ZREG >> (STAGE - 1)) & 1) && NB == 16 && !ORCHA_ONEBAR && !ORCHA_XSHFL &&
                                SZ <= NW && SZ * (ROUNDS - 1) + (NW - SZ) * ROUNDS >= SX + SY;
+  // ZREG with one x, one y and (warps < SZ) one z slot per warp: the phase-1
+  // schedule is static (ORCHA_STATIC3; measured 1.011 vs 1.007 ms for stage 2:
+  // off)
+  static constexpr bool STATIC3 = ORCHA_STATIC3 && ZREG && SX == NW && SY == NW && ROUNDS == 3 && FZ % 32 == 0;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
   // (+ the gather mode's per-row sources of the three z classes, 3 x IR x 16 B: SMEM_G)
   static constexpr size_t SMEM =
@@ -657,6 +664,10 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
     tbase[r] = (ORCHA_XSHFL && kind == 0) ? xbase : kind < 3 ? task_base(kind, t) : 0;
   }
 
+  // Gm::STATIC3: this thread's x and y faces (clamped to the last face)
+  const int sx_t = min(warp * 32 + lane, Gm::FX - 1), sy_t = min(warp * 32 + lane, Gm::FY - 1);
+  const int sx_b = Gm::STATIC3 ? task_base(0, sx_t) : 0, sy_b = Gm::STATIC3 ? task_base(1, sy_t) : 0;
+  const int sz_b = Gm::STATIC3 && tid < Gm::FZ ? task_base(2, tid) : 0;
   bool writes_faces = false;
 #pragma unroll
   for (int r = 0; r < Gm::ROUNDS; r++) writes_faces |= tkind[r] < 3;
@@ -767,6 +778,14 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
     // phase 1: all face fluxes of the band's plane k (inputs: planes it+1 .. it+4)
     double* fz_cur = Fz + (it & 1) * 5 * Gm::FZ;
     if (ORCHA_ONEBAR && it > 0 && writes_faces) mbar_wait(fdone, (it - 1) & 1);  // update(it-1) read the faces
+    if constexpr (Gm::STATIC3) {
+      // every warp: x slot `warp`, y slot `warp`, z slot `warp` (w < SZ), in
+      // straight-line code the compiler may interleave; the lanes past the
+      // last face of a slot recompute (and store) that face
+      x_task(sx_t, sx_b, it);
+      y_task(sy_t, sy_b, it);
+      if (warp < Gm::SZ) z_task(tid, sz_b, it, zf_cur);
+    } else {
 #pragma unroll
     for (int r = 0; r < Gm::ROUNDS; r++) {
       if (tkind[r] == 0) x_task(ttask[r], tbase[r], it);
@@ -776,6 +795,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
         if constexpr (Gm::ZREG) z_task(ttask[r], tbase[r], it, zf_cur);
         else z_task(ttask[r], tbase[r], it, fz_cur);
       }
+    }
     }
     constexpr int UW = UWARPS;
     // the EOS of plane it+5 (read from iteration it+1 on; its copy was issued

@@ -1091,27 +1091,76 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
 // cubes.  Stage-1 cell-stages per cell-update on cfg4 (16^3 blocks, 16^3
 // of them, outflow): 1.95 computed ring, 1.15 borrowed (1.0 away from self
 // sides; 3.4 -> 1.0 at 8^3).
+template <int NB, int SCH, bool GT>
+static cudaError_t hybrid_attrs_g() {
+  constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
+  cudaError_t e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, GT, SCH, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 0>::SMEM_G);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 1, 0, GT, SCH, 1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM_G);
+  if constexpr (NB == 16) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / S>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>::SMEM_G);
+  }
+  return e;
+}
+
 template <int NB, int SCH>
 static cudaError_t hybrid_attrs() {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
   static cudaError_t once = [] {
-    cudaError_t e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 0>::SMEM_G);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM_G);
+    cudaError_t e = hybrid_attrs_g<NB, SCH, true>();
+    if (e == cudaSuccess) e = hybrid_attrs_g<NB, SCH, false>();
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 2, S, 0>::SMEM);
-    if constexpr (NB == 16) {
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1, NB + 2, (NB + 2) / S>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>::SMEM_G);
-    }
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 2, S, 0, 0, false, SCH, 0>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 2, S, 0>::SMEM);
     return e;
   }();
   return once;
+}
+
+// The stage-1 launches of the borrowed ring over the slot map: the box, the
+// 18 x 18 kernel (16^3) and the interior kernel; GT: the gather-mode staging
+// (one packet, x-guards only filled) or the packet's own materialised guards
+// (full fill: several packets per set, each with its own slot map).
+template <int NB, int SCH, bool GT>
+static void launch_hyb_stage1(const DevGrid& G, double* state, double* u1, const SlotInfo* slots, const int* smap,
+                              const int* nb4, int nint, const PushEntry* hpush, const NbrEntry* nbr,
+                              const double* d_dt, double h_dt, DtRecord* records, DevStatus* st, cudaStream_t sb,
+                              cudaStream_t s) {
+  constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
+  const int* sm = smap;
+  // the box (two x or two y self sides: a one-block-wide brick; every NB)
+  if (nb4[0] > 0) {
+    stage_fused_kernel<NB, 1, S, 0, 0, GT, SCH, 1>
+        <<<nb4[0] * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records,
+                                                                            st, hpush, nbr, sm);
+    count_launch();
+  }
+  sm += nb4[0];
+  if constexpr (NB == 16) {
+    // at most one self side per axis: 18 x 18 output columns / rows, the
+    // 2 ring columns (rows) on the self side, or one on each side of an
+    // axis without one (computed, not stored)
+    if (nb4[1] > 0) {
+      using GC = Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>;
+      stage_fused_kernel<NB, 1, S, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / S>
+          <<<nb4[1] * S, GC::NT, GC::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
+      count_launch();
+    }
+    sm += nb4[1];
+  }
+  if (nint > 0) {
+    stage_fused_kernel<NB, 1, S, 1, 0, GT, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM_G, s>>>(
+        G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
+    count_launch();
+  }
 }
 
 template <int NB, int SCH>
@@ -1138,32 +1187,10 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
       if (e != cudaSuccess) return e;
     }
     cudaStream_t sb = fork ? side : s;
-    const int* sm = smap;
-    // the box (two x or two y self sides: a one-block-wide brick; every NB)
-    if (nb4[0] > 0) {
-      stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1>
-          <<<nb4[0] * S, Geo<NB, 1, S, 0>::NT, Geo<NB, 1, S, 0>::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt,
-                                                                              records, st, hpush, nbr, sm);
-      count_launch();
-    }
-    sm += nb4[0];
-    if constexpr (NB == 16) {
-      // at most one self side per axis: 18 x 18 output columns / rows, the
-      // 2 ring columns (rows) on the self side, or one on each side of an
-      // axis without one (computed, not stored)
-      if (nb4[1] > 0) {
-        using GC = Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>;
-        stage_fused_kernel<NB, 1, S, 0, 0, true, SCH, 1, NB + 2, (NB + 2) / S>
-            <<<nb4[1] * S, GC::NT, GC::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
-        count_launch();
-      }
-      sm += nb4[1];
-    }
-    if (nint > 0) {
-      stage_fused_kernel<NB, 1, S, 1, 0, true, SCH, 1><<<nint * S, Geo<NB, 1, S, 1>::NT, Geo<NB, 1, S, 1>::SMEM_G, s>>>(
-          G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
-      count_launch();
-    }
+    if (nbr) launch_hyb_stage1<NB, SCH, true>(G, state, u1, slots, smap, nb4, nint, hpush, nbr, d_dt, h_dt, records,
+                                              st, sb, s);
+    else launch_hyb_stage1<NB, SCH, false>(G, state, u1, slots, smap, nb4, nint, hpush, nbr, d_dt, h_dt, records, st,
+                                           sb, s);
     if (fork) {
       e = cudaEventRecord(ev_join, side);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_join, 0);
@@ -1172,8 +1199,12 @@ static cudaError_t launch_hybrid_nb(const DevGrid& G, double* state, double* u1,
   }
   if (parts & 2) {
     PhaseScope ph(PH_STAGE2, s);
-    stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0><<<nslots * S, Geo<NB, 2, S, 0>::NT, Geo<NB, 2, S, 0>::SMEM, s>>>(
-        G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr, nullptr);
+    if (push)  // gather mode: U^{n+1} into the x-guards too (the next fill launches nothing)
+      stage_fused_kernel<NB, 2, S, 0, 2, false, SCH, 0><<<nslots * S, Geo<NB, 2, S, 0>::NT, Geo<NB, 2, S, 0>::SMEM, s>>>(
+          G, state, u1, slots, d_dt, h_dt, records, st, push, nullptr, nullptr);
+    else
+      stage_fused_kernel<NB, 2, S, 0, 0, false, SCH, 0><<<nslots * S, Geo<NB, 2, S, 0>::NT, Geo<NB, 2, S, 0>::SMEM, s>>>(
+          G, state, u1, slots, d_dt, h_dt, records, st, nullptr, nullptr, nullptr);
     count_launch();
     *nrecords = (long long)nslots * S;
   }

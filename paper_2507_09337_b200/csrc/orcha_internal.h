@@ -133,6 +133,7 @@ struct orcha_packet {
   const orcha::PushEntry* d_push;     // targets in the states
   const orcha::PushEntry* d_push_u1;  // targets in the stage-1 buffers
   const FillPlan* push_plan;          // the plan those tables belong to
+  int plan_q = -1;                    // this packet's index in push_plan's packet list
   bool guards_pushed;          // the last state update scattered itself into the guards (push_plan)
   bool u1_pushed;              // same for the stage-1 buffer
   bool xguards_pushed;         // the last advance scattered U^{n+1} into the x-guards only (gather mode)

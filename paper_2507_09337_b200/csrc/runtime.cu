@@ -228,6 +228,16 @@ extern "C" int32_t orcha_packet_bytes(const orcha_grid* g, int32_t n, size_t* sb
   return ORCHA_OK;
 }
 
+// Borrowed-ring tables of one packet: the slot map (slots with an x / y self
+// side first -- box, then 18 x 18 -- then the interior ones; each entry slot |
+// self-side mask << 26) and the ring push table (face directions).
+struct HybTables {
+  int* d_smap = nullptr;
+  int nb4[4] = {0, 0, 0, 0};  // box, 18 x 18 (16^3; other sizes: box only), unused, unused
+  int nint = 0;
+  PushEntry* d_push = nullptr;
+};
+
 struct FillPlan {
   std::vector<orcha_packet*> packets;
   std::vector<NbrEntry*> d_tables;   // one per packet (library-owned device memory)
@@ -247,13 +257,9 @@ struct FillPlan {
   SlotFill* d_sf = nullptr;
   SlotFill* d_sf_u1 = nullptr;
   long long nslots_total = 0;
-  // borrowed-ring telescoped step (one packet, not peer mode; fused_impl.cuh
-  // launch_hybrid_nb): the slot map (slots with a self side first, each entry
-  // slot | self-side mask << 26) and the ring push table (face directions)
-  int* d_hyb_smap = nullptr;
-  int hyb_nb4[4] = {0, 0, 0, 0};  // box, 18x18 (16^3; other sizes: box only), unused, unused
-  int hyb_nint = 0;
-  PushEntry* d_hyb_push = nullptr;
+  // borrowed-ring telescoped step (not peer mode; fused_impl.cuh
+  // launch_hybrid_nb), one set of tables per packet
+  std::vector<HybTables> hyb;
 };
 // Frees a plan's device tables and the plan (not its packets' pointers).
 static void free_plan_tables(FillPlan* f) {
@@ -265,8 +271,10 @@ static void free_plan_tables(FillPlan* f) {
   for (auto* t : f->d_cross_u1) cudaFree(t);
   cudaFree(f->d_sf);
   cudaFree(f->d_sf_u1);
-  cudaFree(f->d_hyb_smap);
-  cudaFree(f->d_hyb_push);
+  for (auto& h : f->hyb) {
+    cudaFree(h.d_smap);
+    cudaFree(h.d_push);
+  }
   delete f;
 }
 
@@ -757,62 +765,68 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     f->d_cross.push_back(dx);
     f->d_cross_u1.push_back(dx1);
   }
-  if (npk == 1 && !peer && fused_supported(G) && pk[0]->nslots < (1 << 26)) {
-    // borrowed-ring telescoped step: a side of a block is "self" when its
-    // neighbour is not a resident block of this packet reached by a shift
-    // (physical boundary: clamp / mirror; another rank or packet) -- there
-    // the block computes its stage-1 ring itself, elsewhere it borrows it
-    orcha_packet* p = pk[0];
+  if (!peer && fused_supported(G)) {
+    // borrowed-ring telescoped step, per packet: a side of a block is "self"
+    // when its neighbour is not a resident block of the SAME packet reached by
+    // a shift (physical boundary: clamp / mirror; another rank; another
+    // packet -- its stage 1 runs in another launch) -- there the block
+    // computes its stage-1 ring itself, elsewhere it borrows it
     const long long U1C = fused_u1_cube(G.nb[0]);
-    std::vector<int> grp[4], inr;
-    std::vector<PushEntry> hp((size_t)p->nslots * 27, PushEntry{nullptr, 0, 0});
-    auto local_slot = [&](const int bc[3], const int o[3], int* mode) -> int {
-      HostEntry h = make_entry(g, bc, o);
-      *mode = h.mode;
-      for (int a = 0; a < 3; a++)
-        if (o[a] != 0 && ((h.mode >> (2 * a)) & 3) != kShift) return -1;
-      auto it = where.find(h.src_block);
-      return (it == where.end() || it->second.first != 0) ? -1 : it->second.second;
-    };
-    for (int s = 0; s < p->nslots; s++) {
-      long long b = p->ids[s];
-      int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
-                   (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
-      int mask = 0, md = 0;
-      for (int a = 0; a < 3; a++)
-        for (int sd = 0; sd < 2; sd++) {
-          int o[3] = {0, 0, 0};
-          o[a] = sd ? 1 : -1;
-          const int ns = local_slot(bc, o, &md);
-          if (ns < 0) mask |= 1 << (2 * a + sd);
-          else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
-                   PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
-        }
-      // x / y self sides: the box kernel, or (16^3) the 18 x 18 kernel
-      // when at most one side of each axis is self; none, or z only: the
-      // interior kernel (plane ranges extended on self z sides)
-      const int sx = (mask & 1) + ((mask >> 1) & 1), sy = ((mask >> 2) & 1) + ((mask >> 3) & 1);
-      const int e = s | (mask << 26);
-      if (sx == 0 && sy == 0) inr.push_back(e);
-      else if (G.nb[0] != 16 || sx == 2 || sy == 2) grp[0].push_back(e);
-      else grp[1].push_back(e);
-    }
-    std::vector<int> smap;
-    for (int k = 0; k < 4; k++) {
-      smap.insert(smap.end(), grp[k].begin(), grp[k].end());
-      f->hyb_nb4[k] = (int)grp[k].size();
-    }
-    smap.insert(smap.end(), inr.begin(), inr.end());
-    f->hyb_nint = (int)inr.size();
-    cudaError_t err = cudaMalloc(&f->d_hyb_smap, smap.size() * sizeof(int));
-    if (err == cudaSuccess)
-      err = cudaMemcpy(f->d_hyb_smap, smap.data(), smap.size() * sizeof(int), cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMalloc(&f->d_hyb_push, hp.size() * sizeof(PushEntry));
-    if (err == cudaSuccess)
-      err = cudaMemcpy(f->d_hyb_push, hp.data(), hp.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
-    if (err != cudaSuccess) {
-      free_plan_tables(f);
-      return cuda_fail(err, "upload borrowed-ring tables");
+    f->hyb.resize(npk);
+    for (int q = 0; q < npk; q++) {
+      orcha_packet* p = pk[q];
+      if (p->nslots >= (1 << 26)) continue;
+      HybTables& ht = f->hyb[q];
+      std::vector<int> grp[4], inr;
+      std::vector<PushEntry> hp((size_t)p->nslots * 27, PushEntry{nullptr, 0, 0});
+      auto local_slot = [&](const int bc[3], const int o[3], int* mode) -> int {
+        HostEntry h = make_entry(g, bc, o);
+        *mode = h.mode;
+        for (int a = 0; a < 3; a++)
+          if (o[a] != 0 && ((h.mode >> (2 * a)) & 3) != kShift) return -1;
+        auto it = where.find(h.src_block);
+        return (it == where.end() || it->second.first != q) ? -1 : it->second.second;
+      };
+      for (int s = 0; s < p->nslots; s++) {
+        long long b = p->ids[s];
+        int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
+                     (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+        int mask = 0, md = 0;
+        for (int a = 0; a < 3; a++)
+          for (int sd = 0; sd < 2; sd++) {
+            int o[3] = {0, 0, 0};
+            o[a] = sd ? 1 : -1;
+            const int ns = local_slot(bc, o, &md);
+            if (ns < 0) mask |= 1 << (2 * a + sd);
+            else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
+                     PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
+          }
+        // x / y self sides: the box kernel, or (16^3) the 18 x 18 kernel
+        // when at most one side of each axis is self; none, or z only: the
+        // interior kernel (plane ranges extended on self z sides)
+        const int sx = (mask & 1) + ((mask >> 1) & 1), sy = ((mask >> 2) & 1) + ((mask >> 3) & 1);
+        const int e = s | (mask << 26);
+        if (sx == 0 && sy == 0) inr.push_back(e);
+        else if (G.nb[0] != 16 || sx == 2 || sy == 2) grp[0].push_back(e);
+        else grp[1].push_back(e);
+      }
+      std::vector<int> smap;
+      for (int k = 0; k < 4; k++) {
+        smap.insert(smap.end(), grp[k].begin(), grp[k].end());
+        ht.nb4[k] = (int)grp[k].size();
+      }
+      smap.insert(smap.end(), inr.begin(), inr.end());
+      ht.nint = (int)inr.size();
+      cudaError_t err = cudaMalloc(&ht.d_smap, smap.size() * sizeof(int));
+      if (err == cudaSuccess)
+        err = cudaMemcpy(ht.d_smap, smap.data(), smap.size() * sizeof(int), cudaMemcpyHostToDevice);
+      if (err == cudaSuccess) err = cudaMalloc(&ht.d_push, hp.size() * sizeof(PushEntry));
+      if (err == cudaSuccess)
+        err = cudaMemcpy(ht.d_push, hp.data(), hp.size() * sizeof(PushEntry), cudaMemcpyHostToDevice);
+      if (err != cudaSuccess) {
+        free_plan_tables(f);
+        return cuda_fail(err, "upload borrowed-ring tables");
+      }
     }
   }
   if (npk > 1) {
@@ -868,6 +882,12 @@ static int32_t fill_impl(orcha_packet* const* pk, int32_t npk, orcha_comm* comm,
 }
 
 static cudaError_t hyb_side(orcha_packet* p);
+// Borrowed ring: the box / 18 x 18 and interior stage-1 kernels of a packet
+// go on two streams when both are big enough for the overlap to pay for the
+// fork / join (small packets: one stream, no side stream created).
+static bool hyb_fork(const HybTables& h) {
+  return h.d_smap && h.nint >= 128 && h.nb4[0] + h.nb4[1] + h.nb4[2] + h.nb4[3] >= 64;
+}
 
 static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* comm, int buffer,
                               bool faces_only, void* stream, int only) {
@@ -975,11 +995,12 @@ static int32_t fill_impl_body(orcha_packet* const* pk, int32_t npk, orcha_comm* 
   }
   for (int q = 0; q < npk; q++) {
     if (only >= 0 && q != only) continue;
-    if (f->d_hyb_smap && q == 0) {  // the borrowed ring's side stream, ahead of the advance
+    if ((size_t)q < f->hyb.size() && hyb_fork(f->hyb[q])) {  // the borrowed ring's side stream, ahead of the advance
       cudaError_t e = hyb_side(pk[q]);
       if (e != cudaSuccess) return cuda_fail(e, "side stream");
     }
     pk[q]->d_push = f->d_push[q];
+    pk[q]->plan_q = q;
     pk[q]->d_push_u1 = f->d_push_u1[q];
     pk[q]->push_plan = f;
     pk[q]->peer_comm = buffer ? pk[q]->peer_comm : f->peer;
@@ -1198,6 +1219,18 @@ static cudaError_t hyb_side(orcha_packet* p) {
   return e;
 }
 
+// The borrowed-ring tables of packet p's current plan, if its step can use
+// them: the gather-mode fill of a one-packet set (x-guard push by stage 2),
+// or the full fill (no guard push); not the guard-push mode.
+static const HybTables* hyb_tables(const orcha_packet* p, bool xpush, const PushEntry* push) {
+  if (ring_mode() != 1 || !p->push_plan || (push && !xpush)) return nullptr;
+  const FillPlan* f = p->push_plan;
+  const int q = p->plan_q;
+  if (q < 0 || (size_t)q >= f->hyb.size() || f->packets[q] != p || !f->hyb[q].d_smap) return nullptr;
+  if (xpush && p->d_nbr != f->d_tables[q]) return nullptr;
+  return &f->hyb[q];
+}
+
 static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, void* stream) {
   if (!p) return fail(ORCHA_E_ARG, "null packet");
   if (!p->guards_valid || !p->guards_full)
@@ -1207,6 +1240,7 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   const DevGrid& G = p->grid->dev;
   cudaError_t e;
   const bool fused = kernel_variant() == 1;
+  const HybTables* hyb = nullptr;
   if (p->guards_xonly && !fused)
     return fail(ORCHA_E_STATE, "the gather-mode fill was done for the fused kernels; refill after changing the variant");
   const PushEntry* push = (fused && push_enabled() && fused_supported(G) && p->push_plan) ? p->d_push : nullptr;
@@ -1217,12 +1251,12 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
   if (!fused)
     e = launch_advance_ref(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
                            p->status, s);
-  else if (!p->peer_comm && xpush && ring_mode() == 1 && p->push_plan->d_hyb_smap &&
-           p->d_nbr == p->push_plan->d_tables[0] && (e = hyb_side(p)) == cudaSuccess)
-    e = launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, p->push_plan->d_hyb_smap,
-                              p->push_plan->hyb_nb4, p->push_plan->hyb_nint, p->push_plan->d_hyb_push, p->d_nbr,
-                              d_dt, h_dt, p->records, &p->nrecords, p->status, s, push, 3,
-                              hyb_concurrent() ? p->side : nullptr, p->ev_ready, p->ev_halo);
+  else if (!p->peer_comm && (hyb = hyb_tables(p, xpush, push)) != nullptr &&
+           (!hyb_fork(*hyb) || (e = hyb_side(p)) == cudaSuccess))
+    e = launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, hyb->d_smap, hyb->nb4, hyb->nint,
+                              hyb->d_push, xpush ? p->d_nbr : nullptr, d_dt, h_dt, p->records, &p->nrecords,
+                              p->status, s, push, 3,
+                              hyb_concurrent() && hyb_fork(*hyb) ? p->side : nullptr, p->ev_ready, p->ev_halo);
   else if (!p->peer_comm)
     e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
                              &p->nrecords, p->status, s, push, p->guards_xonly ? p->d_nbr : nullptr, xpush);
@@ -1342,6 +1376,7 @@ extern "C" int32_t orcha_hydro_step_overlap(orcha_packet* p, orcha_comm* comm, o
   p->d_push = f->d_push[0];
   p->d_push_u1 = f->d_push_u1[0];
   p->push_plan = f;
+  p->plan_q = 0;
   p->guards_valid = true;
   p->guards_xonly = true;
   p->d_nbr = f->d_tables[0];

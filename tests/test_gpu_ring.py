@@ -9,8 +9,9 @@ other side.  The claim is that this is the telescoped step itself: the parity
 build is bitwise the oracle's telescoped mode (state, dt and argmax every
 step) for every boundary kind, 8^3 / 16^3 / 32^3 blocks, shuffled slot
 orders, one block along an axis, packets with no self side (all periodic) and
-with only self sides, the F4 scheme variants, supersonic flow, and virtual
-ranks (remote sides are self sides).  The production build is checked against
+with only self sides, the F4 scheme variants, supersonic flow, virtual ranks
+(remote sides are self sides), several packets per device and the full fill
+mode (sides towards another packet are self sides).  The production build is checked against
 the oracle by the c13 metric and against the literal ring (mode 0)."""
 import numpy as np
 import pytest
@@ -143,3 +144,47 @@ def test_virtual_ranks_parity_build_equals_oracle():
     Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4)
     assert [x[0] for x in logB] == olog.dts
     assert np.array_equal(B, Oo)
+
+
+@pytest.mark.parametrize("npackets,shuffle", [(2, False), (3, True), (5, True)])
+@pytest.mark.parametrize("name", ["mixed16", "mixed8", "sedov16_4", "all_periodic"])
+def test_multi_packet_parity_build_equals_oracle(name, npackets, shuffle):
+    # several packets per device (full fill mode): a side towards another
+    # packet is a self side (that packet's stage 1 is another launch)
+    nb, nblk, bc, ic, steps = CASES[name]
+    g = H.make_grid(3, nb, nblk, bc=bc, parity=True)
+    U0 = _ic(ic, g.N, seed=65)
+    G, t, log, pk = H.gpu_run(g, U0, nsteps=steps, npackets=npackets, shuffle=shuffle)
+    Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=steps)
+    assert [x[0] for x in log] == olog.dts
+    assert np.array_equal(G, Oo)
+
+
+@pytest.mark.parametrize("name", ["mixed16", "mixed32"])
+def test_full_fill_one_packet_parity_build_equals_oracle(name):
+    # the borrowed ring over the packet's materialised guards (no gather)
+    from paper_2507_09337_b200 import abi
+    nb, nblk, bc, ic, steps = CASES[name]
+    g = H.make_grid(3, nb, nblk, bc=bc, parity=True)
+    abi.call(g.lib, "orcha_set_fill_mode", 0)
+    U0 = _ic(ic, g.N, seed=66)
+    G, t, log, pk = H.gpu_run(g, U0, nsteps=steps)
+    Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=steps)
+    assert [x[0] for x in log] == olog.dts
+    assert np.array_equal(G, Oo)
+
+
+def test_multi_packet_production_against_literal_ring():
+    nb, nblk, bc, ic, steps = CASES["sedov16_4"]
+    g = H.make_grid(3, nb, nblk, bc=bc)
+    U0 = _ic(ic, g.N, seed=67)
+    try:
+        _ring(g.lib, 0)
+        B, _, logB, _ = H.gpu_run(g, U0, nsteps=steps, npackets=4)
+        _ring(g.lib, 1)
+        A, _, logA, _ = H.gpu_run(g, U0, nsteps=steps, npackets=4)
+    finally:
+        _ring(g.lib, 1)
+    assert H.parity_error(A, B) <= 1e-12, H.error_report(A, B)
+    for a, b in zip(logA, logB):
+        assert abs(a[0] - b[0]) <= 1e-13 * b[0] and a[2] == b[2]

@@ -699,6 +699,17 @@ def main():
         variants["per-stage"]["note"] = ("fill -> dt -> stage 1 (interior) -> U1 guard refill -> stage 2; "
                                          "oracle mode 'refill'; gather fill mode: no fill kernel runs (stage 1 "
                                          "writes the U1 x-guards, stage 2 stages U1 guard rows from their owners)")
+        # the paper's literal telescoped step (stage-1 ring computed on every
+        # side, orcha_set_ring_mode(0)) with the same kernels -- the same result
+        if lib.orcha_get_ring_mode() == 1:
+            lib.orcha_set_ring_mode(0)
+            try:
+                variants["literal-ring"] = timed_variant("telescoped", args.steps)
+            finally:
+                lib.orcha_set_ring_mode(1)
+            variants["literal-ring"]["note"] = ("orcha_set_ring_mode(0): every block computes its whole 2-cell "
+                                               "stage-1 ring (box kernel, 1498 fp64 per cell-update) -- the "
+                                               "main line's result, with the ring borrowed from resident owners")
         # restore the packet to a telescoped-step history is not needed: both
         # variants advance the same Sedov state, timing only
     if args.method == "telescoped" and not args.no_variants and clock is not None and world == 1:

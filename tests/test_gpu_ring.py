@@ -188,3 +188,43 @@ def test_multi_packet_production_against_literal_ring():
     assert H.parity_error(A, B) <= 1e-12, H.error_report(A, B)
     for a, b in zip(logA, logB):
         assert abs(a[0] - b[0]) <= 1e-13 * b[0] and a[2] == b[2]
+
+
+@pytest.mark.parametrize("name,npackets", [("mixed16", 1), ("mixed8", 1), ("sedov16_4", 3), ("one_along_x", 1)])
+def test_every_u1_cell_stage2_reads_is_written_each_step(name, npackets):
+    # the U1 cubes are poisoned (NaN bytes) before every advance: a stage-2
+    # read of a ring cell that no stage-1 launch of this step wrote (neither
+    # the block on a self side nor the owner's push) would spread NaN
+    import math
+    import torch
+    from paper_2507_09337_b200 import hydro
+    nb, nblk, bc, ic, steps = CASES[name]
+    g = H.make_grid(3, nb, nblk, bc=bc, parity=True)
+    U0 = _ic(ic, g.N, seed=68)
+    pk = H.gpu_setup(g, U0, npackets, shuffle=True)
+    u1_cube = ((nb[0] + 4) ** 3 * 8 + 255) // 256 * 256
+    dts = []
+    for _ in range(4):
+        hydro.orcha_fill_guardcells(pk)
+        info = hydro.orcha_compute_dt(pk, math.inf)
+        for p in pk:
+            p.scratch[: len(p.block_ids) * 5 * u1_cube].fill_(0xFF)
+        for p in pk:
+            hydro.orcha_hydro_advance(p, info.dt)
+        dts.append(info.dt)
+    torch.cuda.synchronize()
+    G = H.gather(g, pk)
+    Oo, olog = H.oracle_run(H.oracle_grid(g), U0, nsteps=4)
+    assert dts == olog.dts
+    assert np.array_equal(G, Oo)
+
+
+def test_production_run_is_deterministic():
+    # each U1 cell has one writer per step (the block, or the owner's push;
+    # the two stage-1 launches run concurrently on two streams): two runs agree
+    # (cfg3: 512 blocks, 216 interior -- large enough for the two-stream launch)
+    g = H.make_grid(3, (16, 16, 16), (8, 8, 8), bc=((O, O),) * 3)
+    U0 = inp.sedov(g.N)
+    A = H.gpu_run(g, U0, nsteps=8)[0]
+    B = H.gpu_run(g, U0, nsteps=8)[0]
+    assert np.array_equal(A, B)

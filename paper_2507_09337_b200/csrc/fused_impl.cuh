@@ -253,7 +253,11 @@ struct Geo {
   static constexpr int MINB_S = (int)(ORCHA_SMEM_PER_SM / (SMEM + 1024));
   static constexpr int MINB_R = 65536 / (NT * (ZREG ? 120 : 80));  // at ~80 registers per thread (~120 with ZREG)
   static constexpr int MINB_SR = MINB_S < MINB_R ? MINB_S : MINB_R;
-  static constexpr int MINB = MINB_SR < 1 ? 1 : (MINB_SR > 8 ? 8 : MINB_SR);
+#ifndef ORCHA_ST2_MINB  // experiments: CTAs per SM the stage-2 kernels are compiled for
+#define ORCHA_ST2_MINB 0
+#endif
+  static constexpr int MINB = (STAGE == 2 && ORCHA_ST2_MINB) ? ORCHA_ST2_MINB
+                              : MINB_SR < 1 ? 1 : (MINB_SR > 8 ? 8 : MINB_SR);
   static_assert(NT >= FZ, "one update cell per thread");
   static_assert((BAND * 8) % 16 == 0, "bulk copies need 16-byte multiples");
 };

@@ -120,6 +120,11 @@
 #ifndef ORCHA_ZREG
 #define ORCHA_ZREG 2
 #endif
+// row bands per 16^3 block of the borrowed ring's 18 x 18 stage-1 kernel (3: 6-row
+// bands, 3 CTAs per SM; 2.205 vs 2.217 ms per cfg4 step with 2, profiles/r02_ab_trim3.txt)
+#ifndef ORCHA_TRIM_SPLIT
+#define ORCHA_TRIM_SPLIT 3
+#endif
 #ifndef ORCHA_STATIC3
 #define ORCHA_STATIC3 0
 #endif
@@ -1105,9 +1110,10 @@ static cudaError_t hybrid_attrs_g() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM_G);
   if constexpr (NB == 16) {
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / S>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>::SMEM_G);
+      e = cudaFuncSetAttribute(
+          stage_fused_kernel<NB, 1, ORCHA_TRIM_SPLIT, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / ORCHA_TRIM_SPLIT>,
+          cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)Geo<NB, 1, ORCHA_TRIM_SPLIT, 0, NB + 2, (NB + 2) / ORCHA_TRIM_SPLIT>::SMEM_G);
   }
   return e;
 }
@@ -1153,9 +1159,10 @@ static void launch_hyb_stage1(const DevGrid& G, double* state, double* u1, const
     // 2 ring columns (rows) on the self side, or one on each side of an
     // axis without one (computed, not stored)
     if (nb4[1] > 0) {
-      using GC = Geo<NB, 1, S, 0, NB + 2, (NB + 2) / S>;
-      stage_fused_kernel<NB, 1, S, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / S>
-          <<<nb4[1] * S, GC::NT, GC::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
+      constexpr int ST = ORCHA_TRIM_SPLIT;
+      using GC = Geo<NB, 1, ST, 0, NB + 2, (NB + 2) / ST>;
+      stage_fused_kernel<NB, 1, ST, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / ST>
+          <<<nb4[1] * ST, GC::NT, GC::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);
       count_launch();
     }
     sm += nb4[1];

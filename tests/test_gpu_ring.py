@@ -70,9 +70,10 @@ def test_parity_build_equals_oracle_telescoped(name, shuffle):
     assert np.array_equal(G, Oo)
 
 
+@pytest.mark.parametrize("nb,nblk", [((16, 16, 16), (3, 2, 2)), ((8, 8, 8), (4, 3, 2)), ((32, 32, 32), (2, 1, 2))])
 @pytest.mark.parametrize("variant", [dict(riemann=1), dict(limiter=1), dict(eos=1, eos_work=1, arad=1e-3)])
-def test_parity_build_scheme_variants(variant):
-    g = H.make_grid(3, (16, 16, 16), (3, 2, 2), bc=((O, R), (P, P), (R, O)), parity=True, **variant)
+def test_parity_build_scheme_variants(variant, nb, nblk):
+    g = H.make_grid(3, nb, nblk, bc=((O, R), (P, P), (R, O)), parity=True, **variant)
     _ring(g.lib, 1)
     U0 = inp.supersonic_field(g.N, seed=62)
     G, t, log, pk = H.gpu_run(g, U0, nsteps=4)

@@ -125,6 +125,13 @@
 #ifndef ORCHA_TRIM_SPLIT
 #define ORCHA_TRIM_SPLIT 3
 #endif
+// Stage 2 with one CTA barrier per plane (ORCHA_PIPE2): double-buffered x / y
+// face arrays, so the faces of plane k+1 need not wait for the updates of
+// plane k; the z-face tasks (the only readers of the plane converted in
+// phase 2) wait for that EOS on an mbarrier instead of the end-of-plane barrier
+#ifndef ORCHA_PIPE2
+#define ORCHA_PIPE2 0
+#endif
 #ifndef ORCHA_STATIC3
 #define ORCHA_STATIC3 0
 #endif
@@ -241,10 +248,12 @@ struct Geo {
   // schedule is static (ORCHA_STATIC3; measured 1.011 vs 1.007 ms for stage 2:
   // off)
   static constexpr bool STATIC3 = ORCHA_STATIC3 && ZREG && SX == NW && SY == NW && ROUNDS == 3 && FZ % 32 == 0;
+  static constexpr bool PIPE = ORCHA_PIPE2 && STAGE == 2 && ZREG && !ORCHA_ONEBAR;
   // + mbarriers (NS x 8 B) + per-staged-row sign-flip masks (NS x IR bytes, gather mode)
   // (+ the gather mode's per-row sources of the three z classes, 3 x IR x 16 B: SMEM_G)
   static constexpr size_t SMEM =
-      sizeof(double) * (size_t)(NS * 5 * BAND + 5 * FX + 5 * FY + (ZREG ? 0 : 2 * 5 * FZ + (ZC ? 5 * FZ : 0))) + 64 +
+      sizeof(double) * (size_t)(NS * 5 * BAND + (PIPE ? 2 : 1) * 5 * (FX + FY) +
+                                (ZREG ? 0 : 2 * 5 * FZ + (ZC ? 5 * FZ : 0))) + 64 +
       ((NS * IR + 15) / 16) * 16;
   // gather-mode instantiations also hold the per-row sources (kept out of
   // the plain kernels: 576 more bytes pushed the telescoped stage 2's 3 CTAs
@@ -376,9 +385,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
   };
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;                                   // [NS][5][IR][IPX]
-  double* Fx = ring + NS * 5 * BAND;                     // [5][H][W+1]
-  double* Fy = Fx + 5 * Gm::FX;                          // [5][H+1][W]
-  double* Fz = Fy + 5 * Gm::FY;                          // [2][5][H][W] (not with Gm::ZREG)
+  double* const FxA = ring + NS * 5 * BAND;              // [5][H][W+1] (x2: Gm::PIPE)
+  double* const FyA = FxA + 5 * Gm::FX;                  // [5][H+1][W]
+  double* Fx = FxA;                                      // this plane's (Gm::PIPE: buffer it & 1)
+  double* Fy = FyA;
+  double* Fz = FyA + 5 * Gm::FY + (Gm::PIPE ? 5 * (Gm::FX + Gm::FY) : 0);  // [2][5][H][W] (not with Gm::ZREG)
   double* Zc = Fz + (Gm::ZREG ? 0 : 2 * 5 * Gm::FZ);     // [5][H][W] z-face carry (Gm::ZC, not Gm::ZREG)
   uint64_t* bar = reinterpret_cast<uint64_t*>(Zc + (Gm::ZC && !Gm::ZREG ? 5 * Gm::FZ : 0));
   // Gm::ZREG: this thread's z-face fluxes (k-1/2 and k+1/2) and carried face state
@@ -786,6 +797,10 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
     }
     // phase 1: all face fluxes of the band's plane k (inputs: planes it+1 .. it+4)
     double* fz_cur = Fz + (it & 1) * 5 * Gm::FZ;
+    if constexpr (Gm::PIPE) {
+      Fx = FxA + (it & 1) * 5 * (Gm::FX + Gm::FY);
+      Fy = Fx + 5 * Gm::FX;
+    }
     if (ORCHA_ONEBAR && it > 0 && writes_faces) mbar_wait(fdone, (it - 1) & 1);  // update(it-1) read the faces
     if constexpr (Gm::STATIC3) {
       // every warp: x slot `warp`, y slot `warp`, z slot `warp` (w < SZ), in
@@ -800,7 +815,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
       if (tkind[r] == 0) x_task(ttask[r], tbase[r], it);
       else if (tkind[r] == 1) y_task(ttask[r], tbase[r], it);
       else if (tkind[r] == 2) {
-        if (ORCHA_ONEBAR == 2 && it > 0) mbar_wait(cdone, (it - 1) & 1);  // plane it+4 converted
+        if ((ORCHA_ONEBAR == 2 || Gm::PIPE) && it > 0) mbar_wait(cdone, (it - 1) & 1);  // plane it+4 converted
         if constexpr (Gm::ZREG) z_task(ttask[r], tbase[r], it, zf_cur);
         else z_task(ttask[r], tbase[r], it, fz_cur);
       }
@@ -821,7 +836,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
           convert(it + 5);
         }
       }
-      if (ORCHA_ONEBAR == 2 && (!CSPLIT || warp >= UW)) {  // plane it+5 is primitives
+      if ((ORCHA_ONEBAR == 2 || Gm::PIPE) && (!CSPLIT || warp >= UW)) {  // plane it+5 is primitives
         __syncwarp();
         if (lane == 0) mbar_arrive(cdone);
       }
@@ -919,7 +934,7 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
         convert(it + 5, CONV_END + tid, UWARPS * 32, NCONV);
       }
     }
-    if (!ORCHA_ONEBAR) __syncthreads();
+    if (!ORCHA_ONEBAR && !Gm::PIPE) __syncthreads();
   }
   if (STAGE == 2) {
     block_reduce_rec<NT>(s_rec, g_rec);

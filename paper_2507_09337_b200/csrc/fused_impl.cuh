@@ -128,7 +128,8 @@
 // Stage 2 with one CTA barrier per plane (ORCHA_PIPE2): double-buffered x / y
 // face arrays, so the faces of plane k+1 need not wait for the updates of
 // plane k; the z-face tasks (the only readers of the plane converted in
-// phase 2) wait for that EOS on an mbarrier instead of the end-of-plane barrier
+// phase 2) wait for that EOS on an mbarrier instead of the end-of-plane barrier.
+// Measured slower (stage 2 1.055 vs 1.009 ms per cfg4 step): off
 #ifndef ORCHA_PIPE2
 #define ORCHA_PIPE2 0
 #endif

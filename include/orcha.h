@@ -346,17 +346,18 @@ int32_t orcha_set_fill_mode(int32_t mode);
 
 /* Ring mode of the telescoped step (sec 6: stage 1 on the block
  * "plus the inner portion of the halo", so stage 2 needs no second guard
- * exchange).  1 = BORROWED (default): in the gather fill mode with one packet
- * (not F2 peer mode), a block computes the stage-1 values of its 2-cell ring
- * only on its "self" sides -- a physical boundary (clamp / mirror), or a
- * neighbour that is not a resident block of the packet (another rank) -- and
- * takes the ring on every other side from the neighbour that owns those
- * cells, whose own stage 1 computes them from the same U^n values: the
- * result is the telescoped step's (bitwise in the parity build), with stage 1
- * on n^3 instead of (n+4)^3 cells away from self sides.  0 = COMPUTED: every
- * block computes its whole ring (the paper's literal scheme).  Other fill
- * modes and packet sets always compute.  ORCHA_RING=0 selects COMPUTED at
- * load.  Errors: ORCHA_E_ARG (mode not 0 / 1). */
+ * exchange).  1 = BORROWED (default): a block computes the stage-1 values of
+ * its 2-cell ring only on its "self" sides -- a physical boundary (clamp /
+ * mirror), or a neighbour that is not a block of the same packet (another
+ * packet, another rank, F2 peer mode's other ranks) -- and takes the ring on
+ * every other side from the neighbour that owns those cells, whose own stage 1
+ * computes them from the same U^n values: the result is the telescoped step's
+ * (bitwise in the parity build), with stage 1 on n^3 instead of (n+4)^3 cells
+ * away from self sides.  0 = COMPUTED: every block computes its whole ring
+ * (the paper's literal scheme).  Applies to the fused 3D kernels in the
+ * gather and full fill modes; the guard-push mode always computes.
+ * ORCHA_RING=0 selects COMPUTED at load.  Errors: ORCHA_E_ARG (mode not 0 /
+ * 1). */
 int32_t orcha_set_ring_mode(int32_t mode);
 int32_t orcha_get_ring_mode(void);
 

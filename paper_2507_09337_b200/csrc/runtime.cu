@@ -765,7 +765,7 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
     f->d_cross.push_back(dx);
     f->d_cross_u1.push_back(dx1);
   }
-  if (!peer && fused_supported(G)) {
+  if (fused_supported(G)) {
     // borrowed-ring telescoped step, per packet: a side of a block is "self"
     // when its neighbour is not a resident block of the SAME packet reached by
     // a shift (physical boundary: clamp / mirror; another rank; another
@@ -1265,13 +1265,28 @@ static int32_t advance_impl(orcha_packet* p, const double* d_dt, double h_dt, vo
     // other ranks' blocks, whose stage 1 reads them: every rank's stage 1
     // ends before any stage 2 starts
     if (!p->guards_xonly || !xpush) return fail(ORCHA_E_STATE, "peer mode: gather-mode fill expected");
-    e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records, &p->nrecords,
-                             p->status, s, push, p->d_nbr, xpush, 1);
+    // the borrowed ring too: the other ranks' sides are self sides (their
+    // rows are read directly by stage 1), the own packet's borrowed
+    hyb = hyb_tables(p, xpush, push);
+    if (hyb && hyb_fork(*hyb)) {
+      e = hyb_side(p);
+      if (e != cudaSuccess) return cuda_fail(e, "side stream");
+    }
+    auto part = [&](int parts) {
+      if (hyb)
+        return launch_advance_hybrid(G, p->state, p->scratch, p->nslots, p->d_slots, hyb->d_smap, hyb->nb4,
+                                     hyb->nint, hyb->d_push, p->d_nbr, d_dt, h_dt, p->records, &p->nrecords,
+                                     p->status, s, push, parts,
+                                     hyb_concurrent() && hyb_fork(*hyb) ? p->side : nullptr, p->ev_ready,
+                                     p->ev_halo);
+      return launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
+                                  &p->nrecords, p->status, s, push, p->d_nbr, xpush, parts);
+    };
+    e = part(1);
     if (e == cudaSuccess) {
       int32_t rc = comm_peer_barrier(p->peer_comm, s);
       if (rc) return rc;
-      e = launch_advance_fused(G, p->state, p->scratch, p->nslots, p->d_slots, d_dt, h_dt, p->records,
-                               &p->nrecords, p->status, s, push, p->d_nbr, xpush, 2);
+      e = part(2);
     }
   }
   if (e != cudaSuccess) return cuda_fail(e, "advance kernels");

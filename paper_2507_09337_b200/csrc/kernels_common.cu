@@ -292,7 +292,9 @@ cudaError_t launch_dt_gather_rec(const DtRecord* r, const DevStatus* st, GatherR
 // The host rule of orcha_compute_dt on the device (same IEEE operations, so
 // bitwise the same dt): combine the ranks' records (max s, ties -> lowest g),
 // dt = cfl / s_max, then the t_end clamp; clock->t advances by dt.
-__global__ void dt_finish_kernel(const GatherRec* all, int nall, double cfl, DevClock* c) {
+__device__ void dt_finish(const GatherRec* all, int nall, double cfl, DevClock* c);
+__global__ void dt_finish_kernel(const GatherRec* all, int nall, double cfl, DevClock* c) { dt_finish(all, nall, cfl, c); }
+__device__ void dt_finish(const GatherRec* all, int nall, double cfl, DevClock* c) {
   double sm = all[0].s;
   long long gm = all[0].g;
   long long bad = 0;
@@ -311,6 +313,36 @@ __global__ void dt_finish_kernel(const GatherRec* all, int nall, double cfl, Dev
   c->nonphysical = bad ? 1 : 0;
   c->t = c->t + dt;
   c->steps = c->steps + 1;
+}
+
+// One packet, one rank: dt_reduce + dt_gather_rec + dt_finish in one launch
+// (the same combine rule, so the same dt, argmax and side outputs: the
+// packet's reduced record `out` and its gather record `grec`).
+__global__ void __launch_bounds__(1024) dt_reduce_finish_kernel(const DtRecord* __restrict__ rec, long long n,
+                                                                DtRecord* out, const DevStatus* st,
+                                                                GatherRec* grec, double cfl, DevClock* c) {
+  double s = -DBL_MAX;
+  long long g = LLONG_MAX;
+  for (long long t = threadIdx.x; t < n; t += blockDim.x) rec_combine(s, g, rec[t].s, rec[t].g);
+  block_reduce_rec<1024>(s, g);
+  if (threadIdx.x == 0) {
+    out->s = s;
+    out->g = g;
+    GatherRec r;
+    r.s = s;
+    r.g = g;
+    r.bad = st->first_bad != ~0ull ? 1 : 0;
+    r.pad = 0;
+    *grec = r;
+    dt_finish(&r, 1, cfl, c);
+  }
+}
+
+cudaError_t launch_dt_reduce_finish(const DtRecord* records, long long n, DtRecord* out, const DevStatus* st,
+                                    GatherRec* grec, double cfl, void* clock, cudaStream_t s) {
+  dt_reduce_finish_kernel<<<1, 1024, 0, s>>>(records, n, out, st, grec, cfl, (DevClock*)clock);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dt_finish(const GatherRec* all, int nall, double cfl, void* clock, cudaStream_t s) {
@@ -362,6 +394,7 @@ cudaError_t common_preload() {
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_reduce_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_gather_rec_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_finish_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, dt_reduce_finish_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, status_reset_kernel);
   return e;
 }

@@ -186,6 +186,8 @@ cudaError_t launch_dt_reduce(const DtRecord* records, long long n, DtRecord* out
 // nall records) dt, tag and the clock update in `clock` (orcha_dev_clock).
 cudaError_t launch_dt_gather_rec(const DtRecord* r, const DevStatus* st, GatherRec* out, cudaStream_t s);
 cudaError_t launch_dt_finish(const GatherRec* all, int nall, double cfl, void* clock, cudaStream_t s);
+cudaError_t launch_dt_reduce_finish(const DtRecord* records, long long n, DtRecord* out, const DevStatus* st,
+                                    GatherRec* grec, double cfl, void* clock, cudaStream_t s);
 cudaError_t launch_dt_reduce_multi(const PacketDt* pd, int npk, DtRecord* out, DevStatus* out_st, cudaStream_t s);
 cudaError_t launch_fill_multi(const DevGrid& G, const SlotFill* sf, long long nslots, cudaStream_t s,
                               int faces_only);

@@ -1178,6 +1178,14 @@ extern "C" int32_t orcha_compute_dt_device(orcha_packet* const* pk, int32_t npk,
   cudaStream_t s = (cudaStream_t)stream;
   GatherRec* mine = nullptr;
   PhaseScope ph(PH_DT, s);
+  if (!comm && npk == 1) {  // one packet, one rank: reduce, record and finish in one launch
+    int32_t rc = ensure_dt_records(pk, npk, s);
+    if (rc) return rc;
+    cudaError_t e = launch_dt_reduce_finish(pk[0]->records, pk[0]->nrecords, pk[0]->result, pk[0]->status,
+                                            pk[0]->d_grec, pk[0]->grid->dev.cfl, d_clock, s);
+    if (e != cudaSuccess) return cuda_fail(e, "dt reduce + finish");
+    return ORCHA_OK;
+  }
   int32_t rc = rank_record(pk, npk, s, &mine);
   if (rc) return rc;
   const GatherRec* all = mine;

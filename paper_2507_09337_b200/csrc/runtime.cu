@@ -1221,7 +1221,17 @@ static bool hyb_concurrent() {
 }
 static cudaError_t hyb_side(orcha_packet* p) {
   if (!hyb_concurrent() || p->side) return cudaSuccess;
-  cudaError_t e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+  // the side stream (blocks with x / y self sides: the longer CTAs) at the
+  // highest stream priority, so their CTAs are dispatched first and the
+  // interior kernel's fill the tail (2.204 -> 2.195 ms per cfg4 step,
+  // profiles/r02_ab_hybprio.txt; ORCHA_HYB_PRIO=0: default priority)
+  static const bool prio = [] {
+    const char* e = getenv("ORCHA_HYB_PRIO");
+    return !(e && atoi(e) == 0);
+  }();
+  int lo = 0, hi = 0;
+  cudaError_t e = prio ? cudaDeviceGetStreamPriorityRange(&lo, &hi) : cudaSuccess;
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, prio ? hi : 0);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_ready, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_halo, cudaEventDisableTiming);
   return e;

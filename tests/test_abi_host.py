@@ -194,3 +194,16 @@ def test_round2_entry_points_validate_arguments_without_device_work(lib):
     assert lib.orcha_fnv1a64(None, 4, ctypes.byref(h)) == E_ARG
     assert "null" in lib.orcha_last_error().decode() or "orcha_fnv1a64" in lib.orcha_last_error().decode()
     lib.orcha_grid_destroy(g)
+
+
+def test_ring_mode_switch_without_device_work(lib):
+    # orcha_set_ring_mode / orcha_get_ring_mode (include/orcha.h): 0 computed,
+    # 1 borrowed (the default); anything else is ORCHA_E_ARG and changes nothing
+    assert lib.orcha_get_ring_mode() in (0, 1)
+    with pytest.raises(abi.OrchaError) as e:
+        abi.call(lib, "orcha_set_ring_mode", 2)
+    assert e.value.status == "ORCHA_E_ARG"
+    abi.call(lib, "orcha_set_ring_mode", 0)
+    assert lib.orcha_get_ring_mode() == 0
+    abi.call(lib, "orcha_set_ring_mode", 1)
+    assert lib.orcha_get_ring_mode() == 1

@@ -148,7 +148,7 @@ def test_virtual_ranks_parity_build_equals_oracle():
 
 
 @pytest.mark.parametrize("npackets,shuffle", [(2, False), (3, True), (5, True)])
-@pytest.mark.parametrize("name", ["mixed16", "mixed8", "sedov16_4", "all_periodic"])
+@pytest.mark.parametrize("name", ["mixed16", "mixed8", "mixed32", "sedov16_4", "all_periodic"])
 def test_multi_packet_parity_build_equals_oracle(name, npackets, shuffle):
     # several packets per device (full fill mode): a side towards another
     # packet is a self side (that packet's stage 1 is another launch)

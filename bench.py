@@ -104,7 +104,7 @@ def borrowed_ring_regions(brick, nb=16):
                 sz = (k == 0) + (k == brick[2] - 1)
                 if not (sx or sy):
                     w = nb
-                elif nb == 16 and sx < 2 and sy < 2:
+                elif nb in (8, 16) and sx < 2 and sy < 2:
                     w = nb + 2
                 else:
                     w = nb + 4

@@ -1131,6 +1131,14 @@ static cudaError_t launch_stage_nb(const DevGrid& G, int stage, double* state, d
 // cubes.  Stage-1 cell-stages per cell-update on cfg4 (16^3 blocks, 16^3
 // of them, outflow): 1.95 computed ring, 1.15 borrowed (1.0 away from self
 // sides; 3.4 -> 1.0 at 8^3).
+// The borrowed ring's (n+2)^2 stage-1 kernel: row bands per block (16^3: 3
+// bands of 6 rows; 8^3: one band of 10); 32^3 blocks keep the box.
+template <int NB>
+struct TrimSplit {
+  static constexpr bool on = NB == 16 || NB == 8;
+  static constexpr int S = NB == 16 ? ORCHA_TRIM_SPLIT : 1;
+};
+
 template <int NB, int SCH, bool GT>
 static cudaError_t hybrid_attrs_g() {
   constexpr int S = NB == 16 ? 2 : NB == 32 ? 4 : 1;
@@ -1139,12 +1147,12 @@ static cudaError_t hybrid_attrs_g() {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(stage_fused_kernel<NB, 1, S, 1, 0, GT, SCH, 1>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Geo<NB, 1, S, 1>::SMEM_G);
-  if constexpr (NB == 16) {
+  if constexpr (TrimSplit<NB>::on) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(
-          stage_fused_kernel<NB, 1, ORCHA_TRIM_SPLIT, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / ORCHA_TRIM_SPLIT>,
+          stage_fused_kernel<NB, 1, TrimSplit<NB>::S, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / TrimSplit<NB>::S>,
           cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (int)Geo<NB, 1, ORCHA_TRIM_SPLIT, 0, NB + 2, (NB + 2) / ORCHA_TRIM_SPLIT>::SMEM_G);
+          (int)Geo<NB, 1, TrimSplit<NB>::S, 0, NB + 2, (NB + 2) / TrimSplit<NB>::S>::SMEM_G);
   }
   return e;
 }
@@ -1185,12 +1193,12 @@ static void launch_hyb_stage1(const DevGrid& G, double* state, double* u1, const
     count_launch();
   }
   sm += nb4[0];
-  if constexpr (NB == 16) {
-    // at most one self side per axis: 18 x 18 output columns / rows, the
-    // 2 ring columns (rows) on the self side, or one on each side of an
+  if constexpr (TrimSplit<NB>::on) {
+    // at most one self side per axis: (n+2) x (n+2) output columns / rows,
+    // the 2 ring columns (rows) on the self side, or one on each side of an
     // axis without one (computed, not stored)
     if (nb4[1] > 0) {
-      constexpr int ST = ORCHA_TRIM_SPLIT;
+      constexpr int ST = TrimSplit<NB>::S;
       using GC = Geo<NB, 1, ST, 0, NB + 2, (NB + 2) / ST>;
       stage_fused_kernel<NB, 1, ST, 0, 0, GT, SCH, 1, NB + 2, (NB + 2) / ST>
           <<<nb4[1] * ST, GC::NT, GC::SMEM_G, sb>>>(G, state, u1, slots, d_dt, h_dt, records, st, hpush, nbr, sm);

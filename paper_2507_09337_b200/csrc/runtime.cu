@@ -801,13 +801,13 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
             else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
                      PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
           }
-        // x / y self sides: the box kernel, or (16^3) the 18 x 18 kernel
+        // x / y self sides: the box kernel, or (16^3, 8^3) the (n+2)^2 kernel
         // when at most one side of each axis is self; none, or z only: the
         // interior kernel (plane ranges extended on self z sides)
         const int sx = (mask & 1) + ((mask >> 1) & 1), sy = ((mask >> 2) & 1) + ((mask >> 3) & 1);
         const int e = s | (mask << 26);
         if (sx == 0 && sy == 0) inr.push_back(e);
-        else if (G.nb[0] != 16 || sx == 2 || sy == 2) grp[0].push_back(e);
+        else if ((G.nb[0] != 16 && G.nb[0] != 8) || sx == 2 || sy == 2) grp[0].push_back(e);
         else grp[1].push_back(e);
       }
       std::vector<int> smap;

@@ -133,6 +133,13 @@
 #ifndef ORCHA_PIPE2
 #define ORCHA_PIPE2 0
 #endif
+// stage 2: the dt epilogue (EOS + signal speed of the new state) of plane k
+// in phase 1 of plane k+1, beside the face tasks (ORCHA_DEFER_DT).  Measured
+// slower (2.29 ms, 2.25 with the static schedule, vs 2.19 per cfg4 step,
+// profiles/r02_ab_deferdt.txt): off
+#ifndef ORCHA_DEFER_DT
+#define ORCHA_DEFER_DT 0
+#endif
 #ifndef ORCHA_LDNA
 #define ORCHA_LDNA 0
 #endif
@@ -775,6 +782,30 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
 
   double s_rec = -DBL_MAX;
   long long g_rec = LLONG_MAX;
+  // stage 2's dt epilogue for one new cell state: the CFL signal speed of the
+  // new state into this thread's record, and the non-physical check
+  auto dt_cell = [&](const double* nw, int k, int ci, int cj) {
+    bool f2;
+    Prim q = (SCH == 0) ? eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2)
+                        : eos_var(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
+    double s = (SCH == 0) ? signal_speed<3>(q, G) : signal_speed_var<3>(q, G);
+    auto gidx = [&]() -> long long {
+      return (((long long)si.bc[2] * NB + k) * G.N[1] + ((long long)si.bc[1] * NB + cj)) * G.N[0] +
+             ((long long)si.bc[0] * NB + ci);
+    };
+    // this thread's cells come in increasing k at a fixed (i, j), so their
+    // global indices increase: dt_better(s, g, s_rec, g_rec) reduces to a
+    // larger s, or the first NaN -- g is formed only when the record moves
+    const bool sn = s != s, rn = s_rec != s_rec;
+    if (sn ? !rn : (!rn && s > s_rec)) { s_rec = s; g_rec = gidx(); }
+    // finite: no exponent field of all ones (integer tests of the high words)
+    bool finite = true;
+#pragma unroll
+    for (int v = 0; v < 5; v++) finite &= (__double2hiint(nw[v]) & 0x7ff00000) != 0x7ff00000;
+    if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)gidx());
+  };
+  double pnw[5];  // ORCHA_DEFER_DT: the last new state whose dt epilogue is pending (plane pk)
+  int pk = -1;
 #pragma unroll 1
   for (int it = 0; it < nk; it++) {
     const int k = kz0 + it;
@@ -818,6 +849,11 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
       Fy = Fx + 5 * Gm::FX;
     }
     if (ORCHA_ONEBAR && it > 0 && writes_faces) mbar_wait(fdone, (it - 1) & 1);  // update(it-1) read the faces
+    if (STAGE == 2 && ORCHA_DEFER_DT && pk >= 0) {  // the previous plane's dt epilogue
+      const int pci = (tid - (tid / W) * W) - ox, pcj = jj0 + tid / W - oy;
+      dt_cell(pnw, pk, pci, pcj);
+      pk = -1;
+    }
     if constexpr (Gm::STATIC3) {
       // every warp: x slot `warp`, y slot `warp`, z slot `warp` (w < SZ), in
       // straight-line code the compiler may interleave; the lanes past the
@@ -923,24 +959,13 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
         for (int v = 0; v < 5; v++) dst[v * cube] = nw[v];
         if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
         if (PUSH == 2) push_x<NB>(G, sxp, ci, cj, k, nw);  // next step's x-guards
-        bool f2;
-        Prim q = (SCH == 0) ? eos(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2)
-                            : eos_var(nw[0], nw[1], nw[2], nw[3], nw[4], G, &f2);
-        double s = (SCH == 0) ? signal_speed<3>(q, G) : signal_speed_var<3>(q, G);
-        auto gidx = [&]() -> long long {
-          return (((long long)si.bc[2] * NB + k) * G.N[1] + ((long long)si.bc[1] * NB + cj)) * G.N[0] +
-                 ((long long)si.bc[0] * NB + ci);
-        };
-        // this thread's cells come in increasing k at a fixed (i, j), so their
-        // global indices increase: dt_better(s, g, s_rec, g_rec) reduces to a
-        // larger s, or the first NaN -- g is formed only when the record moves
-        const bool sn = s != s, rn = s_rec != s_rec;
-        if (sn ? !rn : (!rn && s > s_rec)) { s_rec = s; g_rec = gidx(); }
-        // finite: no exponent field of all ones (integer tests of the high words)
-        bool finite = true;
+        if constexpr (ORCHA_DEFER_DT) {  // the dt epilogue of this cell runs in the next plane's phase 1
 #pragma unroll
-        for (int v = 0; v < 5; v++) finite &= (__double2hiint(nw[v]) & 0x7ff00000) != 0x7ff00000;
-        if (!(nw[0] > 0.0) || !finite) atomicMin(&st->first_bad, (unsigned long long)gidx());
+          for (int v = 0; v < 5; v++) pnw[v] = nw[v];
+          pk = k;
+        } else {
+          dt_cell(nw, k, ci, cj);
+        }
       }
       }
     }
@@ -951,6 +976,10 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
       }
     }
     if (!ORCHA_ONEBAR && !Gm::PIPE) __syncthreads();
+  }
+  if (STAGE == 2 && ORCHA_DEFER_DT && pk >= 0) {
+    const int pci = (tid - (tid / W) * W) - ox, pcj = jj0 + tid / W - oy;
+    dt_cell(pnw, pk, pci, pcj);
   }
   if (STAGE == 2) {
     block_reduce_rec<NT>(s_rec, g_rec);

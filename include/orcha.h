@@ -361,6 +361,20 @@ int32_t orcha_set_fill_mode(int32_t mode);
 int32_t orcha_set_ring_mode(int32_t mode);
 int32_t orcha_get_ring_mode(void);
 
+/* The borrowed ring's classification, on the host (no device work): for a
+ * packet of the n blocks `ids` of grid g taken alone -- a side is "self" when
+ * its face neighbour is not one of these blocks reached by a shift (periodic
+ * wrap included; a clamp / mirror boundary, or a block outside the list, is
+ * self) -- masks[s] = the self sides of block ids[s] (bit 2a: side -a, bit
+ * 2a+1: side +a; axes beyond ndim are self) and groups[s] = its stage-1
+ * kernel: 2 the interior kernel (no x / y self side; planes extended on self
+ * z sides), 1 the (n+2)^2 kernel (16^3 / 8^3 blocks with at most one self
+ * side per x / y axis), 0 the (n+4)^2 box.  The same rule the packet plans
+ * use (several packets: the sides towards the other packets are self).
+ * masks / groups: caller-owned host arrays of n.  Errors: ORCHA_E_ARG (null
+ * pointers, n < 0), ORCHA_E_RANGE (an id outside the grid, or repeated). */
+int32_t orcha_ring_classify(const orcha_grid* g, int32_t n, const int64_t* ids, int32_t* masks, int32_t* groups);
+
 /* Guard push (default OFF -- measured slower than the gather fill on B200,
  * DESIGN.md 6; ORCHA_PUSH=1 in the environment turns it on at load): the
  * fused kernels that produce a new state also scatter each new

@@ -37,7 +37,7 @@ EXPORTS = [
     "orcha_comm_push_dt", "orcha_set_phase_timing", "orcha_phase_times", "orcha_probe_fp64",
     "orcha_fnv1a64", "orcha_comm_peer_register", "orcha_comm_check",
     "orcha_fill_prepare", "orcha_hydro_step_overlap", "orcha_comm_create_ipc", "orcha_comm_ipc_export",
-    "orcha_comm_ipc_attach", "orcha_set_ring_mode", "orcha_get_ring_mode",
+    "orcha_comm_ipc_attach", "orcha_set_ring_mode", "orcha_get_ring_mode", "orcha_ring_classify",
 ]
 
 
@@ -136,6 +136,7 @@ _SIGS = {
     "orcha_set_fill_mode": (_i32, [_i32]),
     "orcha_set_ring_mode": (_i32, [_i32]),
     "orcha_get_ring_mode": (_i32, []),
+    "orcha_ring_classify": (_i32, [_vp, _i32, _P(_i64), _P(_i32), _P(_i32)]),
     "orcha_hydro_stage_devdt": (_i32, [_vp, _i32, _vp, _vp]),
     "orcha_fill_guardcells_stage": (_i32, [_P(_vp), _i32, _vp, _i32, _vp]),
     "orcha_comm_plan": (_i32, [_vp, _i32, _i32, _P(_i32), _i32, _i32, _P(_i64), _i64, _P(_i64)]),

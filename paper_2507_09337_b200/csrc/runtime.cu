@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <functional>
 #include <unordered_map>
 
 #include "comm.h"
@@ -580,6 +581,70 @@ static HostEntry make_entry(const orcha_grid* g, const int bc[3], const int o[3]
   return h;
 }
 
+// Borrowed ring (orcha_set_ring_mode): the self-side mask of block b (bit
+// 2a: side -a, 2a+1: +a) -- a side is self unless its face neighbour is
+// reached by a shift (not across a clamp / mirror boundary) and local_of()
+// gives its slot in the same packet -- and, per side, that slot and the
+// entry's axis modes (-1 on a self side).
+static int ring_sides(const orcha_grid* g, long long b, const std::function<int(long long)>& local_of, int slot6[6],
+                      int mode6[6]) {
+  const DevGrid& G = g->dev;
+  int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]), (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
+  int mask = 0;
+  for (int a = 0; a < 3; a++)
+    for (int sd = 0; sd < 2; sd++) {
+      int o[3] = {0, 0, 0};
+      o[a] = sd ? 1 : -1;
+      const int i = 2 * a + sd;
+      slot6[i] = -1;
+      mode6[i] = 0;
+      if (a >= g->desc.ndim) {
+        mask |= 1 << i;
+        continue;
+      }
+      HostEntry h = make_entry(g, bc, o);
+      const bool shift = ((h.mode >> (2 * a)) & 3) == kShift;
+      const int ns = shift ? local_of(h.src_block) : -1;
+      if (ns < 0) {
+        mask |= 1 << i;
+      } else {
+        slot6[i] = ns;
+        mode6[i] = h.mode;
+      }
+    }
+  return mask;
+}
+
+// The stage-1 kernel group of a block with self-side mask `mask`: 2 = the
+// interior kernel (no x / y self side), 1 = the (n+2)^2 kernel (16^3 and 8^3
+// blocks with at most one self side per x / y axis), 0 = the box.
+static int ring_group(const DevGrid& G, int mask) {
+  const int sx = (mask & 1) + ((mask >> 1) & 1), sy = ((mask >> 2) & 1) + ((mask >> 3) & 1);
+  if (sx == 0 && sy == 0) return 2;
+  if ((G.nb[0] != 16 && G.nb[0] != 8) || sx == 2 || sy == 2) return 0;
+  return 1;
+}
+
+extern "C" int32_t orcha_ring_classify(const orcha_grid* g, int32_t n, const int64_t* ids, int32_t* masks,
+                                       int32_t* groups) {
+  if (!g || n < 0 || (n > 0 && (!ids || !masks || !groups))) return fail(ORCHA_E_ARG, "null argument");
+  std::unordered_map<long long, int> slot;
+  for (int s = 0; s < n; s++) {
+    if (ids[s] < 0 || ids[s] >= g->nblocks) return fail(ORCHA_E_RANGE, "block id out of range");
+    if (!slot.emplace(ids[s], s).second) return fail(ORCHA_E_RANGE, "block listed twice");
+  }
+  auto local_of = [&](long long blk) -> int {
+    auto it = slot.find(blk);
+    return it == slot.end() ? -1 : it->second;
+  };
+  for (int s = 0; s < n; s++) {
+    int ns6[6], md6[6];
+    masks[s] = ring_sides(g, ids[s], local_of, ns6, md6);
+    groups[s] = ring_group(g->dev, masks[s]);
+  }
+  return ORCHA_OK;
+}
+
 static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm, FillPlan** out) {
   const orcha_grid* g = pk_in[0]->grid;
   const DevGrid& G = g->dev;
@@ -779,36 +844,25 @@ static int32_t build_plan(orcha_packet* const* pk_in, int npk, orcha_comm* comm,
       HybTables& ht = f->hyb[q];
       std::vector<int> grp[4], inr;
       std::vector<PushEntry> hp((size_t)p->nslots * 27, PushEntry{nullptr, 0, 0});
-      auto local_slot = [&](const int bc[3], const int o[3], int* mode) -> int {
-        HostEntry h = make_entry(g, bc, o);
-        *mode = h.mode;
-        for (int a = 0; a < 3; a++)
-          if (o[a] != 0 && ((h.mode >> (2 * a)) & 3) != kShift) return -1;
-        auto it = where.find(h.src_block);
+      auto local_of = [&](long long blk) -> int {
+        auto it = where.find(blk);
         return (it == where.end() || it->second.first != q) ? -1 : it->second.second;
       };
       for (int s = 0; s < p->nslots; s++) {
-        long long b = p->ids[s];
-        int bc[3] = {(int)(b % G.nblk[0]), (int)((b / G.nblk[0]) % G.nblk[1]),
-                     (int)(b / ((long long)G.nblk[0] * G.nblk[1]))};
-        int mask = 0, md = 0;
+        int ns6[6], md6[6];
+        const int mask = ring_sides(g, p->ids[s], local_of, ns6, md6);
         for (int a = 0; a < 3; a++)
           for (int sd = 0; sd < 2; sd++) {
+            if (ns6[2 * a + sd] < 0) continue;
             int o[3] = {0, 0, 0};
             o[a] = sd ? 1 : -1;
-            const int ns = local_slot(bc, o, &md);
-            if (ns < 0) mask |= 1 << (2 * a + sd);
-            else hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
-                     PushEntry{p->scratch + (long long)ns * kNVar * U1C, md, 0};
+            hp[(size_t)s * 27 + (o[2] + 1) * 9 + (o[1] + 1) * 3 + (o[0] + 1)] =
+                PushEntry{p->scratch + (long long)ns6[2 * a + sd] * kNVar * U1C, md6[2 * a + sd], 0};
           }
-        // x / y self sides: the box kernel, or (16^3, 8^3) the (n+2)^2 kernel
-        // when at most one side of each axis is self; none, or z only: the
-        // interior kernel (plane ranges extended on self z sides)
-        const int sx = (mask & 1) + ((mask >> 1) & 1), sy = ((mask >> 2) & 1) + ((mask >> 3) & 1);
         const int e = s | (mask << 26);
-        if (sx == 0 && sy == 0) inr.push_back(e);
-        else if ((G.nb[0] != 16 && G.nb[0] != 8) || sx == 2 || sy == 2) grp[0].push_back(e);
-        else grp[1].push_back(e);
+        const int grpk = ring_group(G, mask);
+        if (grpk == 2) inr.push_back(e);
+        else grp[grpk].push_back(e);
       }
       std::vector<int> smap;
       for (int k = 0; k < 4; k++) {

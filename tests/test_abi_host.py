@@ -207,3 +207,74 @@ def test_ring_mode_switch_without_device_work(lib):
     assert lib.orcha_get_ring_mode() == 0
     abi.call(lib, "orcha_set_ring_mode", 1)
     assert lib.orcha_get_ring_mode() == 1
+
+
+def _py_ring_classify(nblk, bc, nb, ids):
+    """The borrowed ring's rule written out independently: a side is self
+    unless its face neighbour is reached by a shift (inside, or a periodic
+    wrap) and is one of `ids`; group 2 interior, 1 the (n+2)^2 kernel (8^3 /
+    16^3, at most one self side per x / y axis), 0 the box."""
+    inset = set(int(b) for b in ids)
+    masks, groups = [], []
+    for b in ids:
+        c = [b % nblk[0], (b // nblk[0]) % nblk[1], b // (nblk[0] * nblk[1])]
+        mask = 0
+        for a in range(3):
+            for sd, o in ((0, -1), (1, 1)):
+                cc = c[a] + o
+                if not 0 <= cc < nblk[a]:
+                    if bc[a][sd] != 1:          # outflow / reflect: no neighbour block
+                        mask |= 1 << (2 * a + sd)
+                        continue
+                    cc %= nblk[a]
+                n = list(c)
+                n[a] = cc
+                if (n[2] * nblk[1] + n[1]) * nblk[0] + n[0] not in inset:
+                    mask |= 1 << (2 * a + sd)
+        sx = (mask & 1) + ((mask >> 1) & 1)
+        sy = ((mask >> 2) & 1) + ((mask >> 3) & 1)
+        masks.append(mask)
+        groups.append(2 if sx == 0 and sy == 0 else 1 if nb in (8, 16) and sx < 2 and sy < 2 else 0)
+    return masks, groups
+
+
+@pytest.mark.parametrize("nb,nblk,bc", [
+    (16, (16, 16, 16), ((0, 0),) * 3),
+    (16, (4, 3, 2), ((1, 1), (0, 2), (1, 1))),
+    (8, (5, 4, 3), ((2, 2), (1, 1), (0, 0))),
+    (32, (3, 2, 2), ((0, 0), (1, 1), (2, 2))),
+    (16, (1, 2, 3), ((1, 1), (1, 1), (0, 0))),
+])
+def test_ring_classify_matches_the_rule(lib, nb, nblk, bc):
+    import numpy as np
+    d = desc(nb=(nb,) * 3, nblk=nblk)
+    for a in range(3):
+        d.bc[a][0], d.bc[a][1] = bc[a]
+    rc, g = create(lib, d)
+    assert rc == 0, lib.orcha_last_error()
+    nblocks = nblk[0] * nblk[1] * nblk[2]
+    rng = np.random.default_rng(5)
+    for ids in (np.arange(nblocks), rng.permutation(nblocks),
+                np.sort(rng.choice(nblocks, size=max(1, nblocks // 2), replace=False))):
+        ids = ids.astype(np.int64)
+        n = len(ids)
+        masks = (ctypes.c_int32 * n)()
+        groups = (ctypes.c_int32 * n)()
+        assert lib.orcha_ring_classify(g, n, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), masks, groups) == 0
+        pm, pg = _py_ring_classify(nblk, bc, nb, ids)
+        assert list(masks) == pm and list(groups) == pg
+    if nblk == (16, 16, 16):  # cfg4's brick: the counts bench.py's work model uses
+        import sys
+        sys.path.insert(0, ROOT)
+        import bench
+        regions = bench.borrowed_ring_regions(nblk)
+        ids = np.arange(nblocks, dtype=np.int64)
+        masks = (ctypes.c_int32 * nblocks)()
+        groups = (ctypes.c_int32 * nblocks)()
+        lib.orcha_ring_classify(g, nblocks, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), masks, groups)
+        w = {2: nb, 1: nb + 2, 0: nb + 4}
+        assert [(w[gr], w[gr], nb + 2 * (((m >> 4) & 1) + ((m >> 5) & 1))) for m, gr in zip(masks, groups)] == regions
+    ids = np.array([0, 0], dtype=np.int64)
+    m2 = (ctypes.c_int32 * 2)()
+    assert lib.orcha_ring_classify(g, 2, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), m2, m2) == -2
+    lib.orcha_grid_destroy(g)

@@ -140,6 +140,11 @@
 #ifndef ORCHA_DEFER_DT
 #define ORCHA_DEFER_DT 0
 #endif
+// borrowed-ring stage 1: the x / y ring-push targets of a thread's column
+// computed once before the plane loop (ORCHA_PUSH_HOIST)
+#ifndef ORCHA_PUSH_HOIST
+#define ORCHA_PUSH_HOIST 1
+#endif
 #ifndef ORCHA_LDNA
 #define ORCHA_LDNA 0
 #endif
@@ -806,6 +811,18 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
   };
   double pnw[5];  // ORCHA_DEFER_DT: the last new state whose dt epilogue is pending (plane pk)
   int pk = -1;
+  // ORCHA_PUSH_HOIST (HYB stage 1): this thread's x / y ring-push targets
+  int hx = -1, hy = -1;
+  if (ORCHA_PUSH_HOIST && HYB && STAGE == 1 && tid < Gm::FZ) {
+    const int hci = (tid - (tid / W) * W) - ox, hcj = jj0 + tid / W - oy;
+    if (hci >= 0 && hci < NB && hcj >= 0 && hcj < NB) {
+      const int xs = hci < 2 ? 0 : (hci >= NB - 2 ? 1 : -1), ys = hcj < 2 ? 2 : (hcj >= NB - 2 ? 3 : -1);
+      if (xs >= 0 && sxp[xs].dst)
+        hx = (int)(sxp[xs].dst - u1) + (2 * (NB + 4) + (hcj + 2)) * (NB + 4) + ((xs ? hci - NB : hci + NB) + 2);
+      if (ys >= 0 && sxp[ys].dst)
+        hy = (int)(sxp[ys].dst - u1) + (2 * (NB + 4) + ((ys == 3 ? hcj - NB : hcj + NB) + 2)) * (NB + 4) + (hci + 2);
+    }
+  }
 #pragma unroll 1
   for (int it = 0; it < nk; it++) {
     const int k = kz0 + it;
@@ -938,7 +955,29 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
 #pragma unroll
           for (int v = 0; v < 5; v++) out[v * U1C] = w[v];
         }
-        push_u1<NB>(sxp, U1C, ci, cj, k, w);
+        if constexpr (ORCHA_PUSH_HOIST) {
+          // x / y targets hoisted out of the plane loop (hx / hy: offsets from
+          // u1 of this column's target at plane 0; -1: none); z per plane
+          if (k >= 0 && k < NB) {
+            constexpr int PL = (NB + 4) * (NB + 4);
+            if (hx >= 0) {
+#pragma unroll
+              for (int v = 0; v < 5; v++) u1[hx + k * PL + v * U1C] = w[v];
+            }
+            if (hy >= 0) {
+#pragma unroll
+              for (int v = 0; v < 5; v++) u1[hy + k * PL + v * U1C] = w[v];
+            }
+            const int zs = k < 2 ? 4 : (k >= NB - 2 ? 5 : -1);
+            if (zs >= 0 && ci >= 0 && ci < NB && cj >= 0 && cj < NB && sxp[zs].dst != nullptr) {
+              double* q = sxp[zs].dst + ((zs == 5 ? k - NB : k + NB) + 2) * PL + (cj + 2) * (NB + 4) + (ci + 2);
+#pragma unroll
+              for (int v = 0; v < 5; v++) q[v * U1C] = w[v];
+            }
+          }
+        } else {
+          push_u1<NB>(sxp, U1C, ci, cj, k, w);
+        }
       } else if (STAGE == 1) {
         double* out = u1 + slot * 5 * U1C + u1_off(ci, cj, k);
 #pragma unroll

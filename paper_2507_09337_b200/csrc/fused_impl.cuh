@@ -811,16 +811,34 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
   };
   double pnw[5];  // ORCHA_DEFER_DT: the last new state whose dt epilogue is pending (plane pk)
   int pk = -1;
+  // ORCHA_PUSH_HOIST, stage 2 with the x-guard push: this thread's target
+  // when it is a shift (gm 1: gx = its offset from `state` at plane 0 -- it
+  // may be negative: another rank's packet in F2 peer mode), a clamp / mirror
+  // target (gm 2: push_x per plane), or none (gm 0)
+  long long gx = 0;
+  int gm = 0;
+  if (ORCHA_PUSH_HOIST && STAGE == 2 && PUSH == 2 && tid < Gm::FZ) {
+    const int gci = (tid - (tid / W) * W) - ox, gcj = jj0 + tid / W - oy;
+    const int side = gci >= NB - 4 ? 1 : (gci < 4 ? 0 : -1);
+    if (side >= 0 && sxp[side].dst != nullptr) {
+      if ((sxp[side].mode & 3) == kShift) {
+        gx = (sxp[side].dst - state) + coff<NB>(side ? gci - NB : gci + NB, gcj, 0);
+        gm = 1;
+      } else {
+        gm = 2;
+      }
+    }
+  }
   // ORCHA_PUSH_HOIST (HYB stage 1): this thread's x / y ring-push targets
-  int hx = -1, hy = -1;
+  long long hx = -1, hy = -1;
   if (ORCHA_PUSH_HOIST && HYB && STAGE == 1 && tid < Gm::FZ) {
     const int hci = (tid - (tid / W) * W) - ox, hcj = jj0 + tid / W - oy;
     if (hci >= 0 && hci < NB && hcj >= 0 && hcj < NB) {
       const int xs = hci < 2 ? 0 : (hci >= NB - 2 ? 1 : -1), ys = hcj < 2 ? 2 : (hcj >= NB - 2 ? 3 : -1);
       if (xs >= 0 && sxp[xs].dst)
-        hx = (int)(sxp[xs].dst - u1) + (2 * (NB + 4) + (hcj + 2)) * (NB + 4) + ((xs ? hci - NB : hci + NB) + 2);
+        hx = (sxp[xs].dst - u1) + (2 * (NB + 4) + (hcj + 2)) * (NB + 4) + ((xs ? hci - NB : hci + NB) + 2);
       if (ys >= 0 && sxp[ys].dst)
-        hy = (int)(sxp[ys].dst - u1) + (2 * (NB + 4) + ((ys == 3 ? hcj - NB : hcj + NB) + 2)) * (NB + 4) + (hci + 2);
+        hy = (sxp[ys].dst - u1) + (2 * (NB + 4) + ((ys == 3 ? hcj - NB : hcj + NB) + 2)) * (NB + 4) + (hci + 2);
     }
   }
 #pragma unroll 1
@@ -997,7 +1015,15 @@ __global__ void __launch_bounds__(Geo<NB, STAGE, SPLIT, MODE, WXT, HT>::NT, Geo<
 #pragma unroll
         for (int v = 0; v < 5; v++) dst[v * cube] = nw[v];
         if (PUSH == 1) push_cell(G, push + slot * 27, ci, cj, k, nw);  // next step's guards
-        if (PUSH == 2) push_x<NB>(G, sxp, ci, cj, k, nw);  // next step's x-guards
+        if (PUSH == 2) {  // next step's x-guards
+          if (ORCHA_PUSH_HOIST && gm == 1) {  // a shift target, hoisted (gx: its offset at plane 0)
+            constexpr int PP = (NB + 8) * (NB + 8);
+#pragma unroll
+            for (int v = 0; v < 5; v++) state[gx + (long long)k * PP + v * cube] = nw[v];
+          } else if (!ORCHA_PUSH_HOIST || gm == 2) {
+            push_x<NB>(G, sxp, ci, cj, k, nw);
+          }
+        }
         if constexpr (ORCHA_DEFER_DT) {  // the dt epilogue of this cell runs in the next plane's phase 1
 #pragma unroll
           for (int v = 0; v < 5; v++) pnw[v] = nw[v];

@@ -60,8 +60,8 @@ FP64_PER_FACE, FP64_PER_EOS = 142.0, 15.0
 # executed thread-instructions per cell-update of the advance kernels (ncu
 # source page of the current kernels) -- the issue-slot view of the same
 # kernels (context beside the fp64 roofline)
-EXEC_INSTR_PER_CU = 2637.4
-EXEC_INSTR_SOURCE = "profiles/r02_sass_mix_ring_v10.txt"
+EXEC_INSTR_PER_CU = 2608.7
+EXEC_INSTR_SOURCE = "profiles/r02_sass_mix_ring_v13.txt"
 
 
 def _stage_counts(w):
